@@ -1,0 +1,618 @@
+/* ntbc_oracle.c -- CPU ORACLE for NTBC inference (arXiv 2407.09543).
+ *
+ * TEST INFRASTRUCTURE ONLY: loaded by tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / reference arm.  Never used by the product path.
+ * Shares no code with paper_2407_09543_b200/ (see ntbc_oracle.h).
+ *
+ * Plain, slow, IEEE-exact C99.  Compiled with -ffp-contract=off so that the
+ * only fused multiply-adds are the explicit fmaf() calls written below; every
+ * other operation is one IEEE-754 binary32 operation rounded to nearest-even.
+ *
+ * Parity status per function:
+ *   all functions below are pinned by -m "not gpu" tests EXCEPT
+ *   o_dot in CHUNK mode, whose summation order is pinned to the
+ *   mathematics only through its error bound (R10).
+ */
+#include "ntbc_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define BC1 1
+#define BC4 4
+#define MAXTEX 8
+#define MAXLV 8
+
+/* ------------------------------------------------------------------------- */
+/* model container                                                            */
+/* ------------------------------------------------------------------------- */
+typedef struct { float s; int32_t z; int res; const uint8_t* q; } o_level;
+typedef struct { int levels, coarsest; o_level lv[MAXLV]; } o_grid;
+typedef struct { int n_layers; int dims[8]; const uint16_t* W[7]; const uint16_t* b[7]; } o_mlp;
+struct o_model {
+    int n_tex, fmt[MAXTEX], hidden, n_hidden, F;
+    o_grid grid[2];        /* 0 = block grid, 1 = texel grid */
+    o_mlp mlp[2];          /* 0 = endpoint net, 1 = colour net */
+    uint8_t* blob;         /* private copy; all pointers above point into it */
+};
+
+static uint32_t rd32(const uint8_t* p) { uint32_t v; memcpy(&v, p, 4); return v; }
+static size_t al16(size_t n) { return (n + 15) & ~(size_t)15; }
+
+int o_model_parse(const void* blob, size_t n, o_model** out) {
+    const uint8_t* b = (const uint8_t*)blob;
+    if (n < 96 || memcmp(b, "NTBC", 4) != 0 || rd32(b + 4) != 1) return -2;
+    o_model* m = (o_model*)calloc(1, sizeof(o_model));
+    m->blob = (uint8_t*)malloc(n);
+    memcpy(m->blob, b, n);
+    b = m->blob;
+    m->n_tex = (int)rd32(b + 8);
+    if (m->n_tex < 1 || m->n_tex > MAXTEX) { o_model_free(m); return -2; }
+    for (int i = 0; i < m->n_tex; i++) {
+        m->fmt[i] = (int)rd32(b + 12 + 4 * i);
+        if (m->fmt[i] != BC1 && m->fmt[i] != BC4) { o_model_free(m); return -2; }
+    }
+    m->hidden = (int)rd32(b + 44); m->n_hidden = (int)rd32(b + 48); m->F = (int)rd32(b + 52);
+    m->grid[0].levels = (int)rd32(b + 56); m->grid[0].coarsest = (int)rd32(b + 60);
+    m->grid[1].levels = (int)rd32(b + 64); m->grid[1].coarsest = (int)rd32(b + 68);
+    int ep_in = (int)rd32(b + 72), n_e = (int)rd32(b + 76), col_in = (int)rd32(b + 80), n_c = (int)rd32(b + 84);
+    if (m->n_hidden < 1 || m->n_hidden > 5 || m->F < 1 || m->grid[0].levels < 1 ||
+        m->grid[0].levels > MAXLV || m->grid[1].levels < 1 || m->grid[1].levels > MAXLV) { o_model_free(m); return -2; }
+    size_t off = 96;
+    const uint8_t* qp = b + off;
+    int nl = m->grid[0].levels + m->grid[1].levels;
+    off += al16((size_t)nl * 8);
+    int li = 0;
+    for (int g = 0; g < 2; g++)
+        for (int l = 0; l < m->grid[g].levels; l++, li++) {
+            o_level* L = &m->grid[g].lv[l];
+            memcpy(&L->s, qp + 8 * li, 4);
+            memcpy(&L->z, qp + 8 * li + 4, 4);
+            L->res = m->grid[g].coarsest << l;
+        }
+    for (int g = 0; g < 2; g++)
+        for (int l = 0; l < m->grid[g].levels; l++) {
+            o_level* L = &m->grid[g].lv[l];
+            size_t sz = (size_t)L->res * L->res * m->F;
+            if (off + sz > n) { o_model_free(m); return -2; }
+            L->q = b + off;
+            off += al16(sz);
+        }
+    int ins[2] = {ep_in, col_in}, outs[2] = {n_e, n_c};
+    for (int k = 0; k < 2; k++) {
+        o_mlp* M = &m->mlp[k];
+        M->n_layers = m->n_hidden + 1;
+        M->dims[0] = ins[k];
+        for (int l = 1; l <= m->n_hidden; l++) M->dims[l] = m->hidden;
+        M->dims[M->n_layers] = outs[k];
+        for (int l = 0; l < M->n_layers; l++) {
+            size_t wsz = (size_t)M->dims[l] * M->dims[l + 1] * 2, bsz = (size_t)M->dims[l + 1] * 2;
+            if (off + al16(wsz) + bsz > n) { o_model_free(m); return -2; }
+            M->W[l] = (const uint16_t*)(b + off); off += al16(wsz);
+            M->b[l] = (const uint16_t*)(b + off); off += al16(bsz);
+        }
+    }
+    int want_e = 0, want_c = 0;
+    for (int i = 0; i < m->n_tex; i++) { want_e += m->fmt[i] == BC1 ? 6 : 2; want_c += m->fmt[i] == BC1 ? 3 : 1; }
+    if (want_e != n_e || want_c != n_c || ep_in != m->grid[0].levels * m->F ||
+        col_in != m->grid[1].levels * m->F) { o_model_free(m); return -2; }
+    *out = m;
+    return 0;
+}
+
+void o_model_free(o_model* m) { if (m) { free(m->blob); free(m); } }
+
+void o_model_info(const o_model* m, int* o) {
+    memset(o, 0, 16 * sizeof(int));
+    o[0] = m->n_tex;
+    for (int i = 0; i < m->n_tex; i++) o[1 + i] = m->fmt[i];
+    o[9] = m->hidden;
+    o[10] = m->mlp[0].dims[m->mlp[0].n_layers];
+    o[11] = m->mlp[1].dims[m->mlp[1].n_layers];
+    o[12] = m->grid[0].levels; o[13] = m->grid[0].coarsest;
+    o[14] = m->grid[1].levels; o[15] = m->grid[1].coarsest;
+}
+
+/* ------------------------------------------------------------------------- */
+/* IEEE binary16 <-> binary32 ("half-precision floating points")       */
+/* ------------------------------------------------------------------------- */
+float o_f16_to_f32(uint16_t h) {
+    int sign = h >> 15, e = (h >> 10) & 31, f = h & 1023;
+    float v;
+    if (e == 0) v = ldexpf((float)f, -24);                 /* subnormal (and zero) */
+    else if (e == 31) v = f ? NAN : INFINITY;
+    else v = ldexpf((float)(1024 + f), e - 25);
+    return sign ? -v : v;
+}
+
+uint16_t o_f32_to_f16(float x) {
+    uint32_t u; memcpy(&u, &x, 4);
+    uint16_t sign = (uint16_t)((u >> 16) & 0x8000);
+    float a = fabsf(x);
+    if (a != a) return (uint16_t)(sign | 0x7e00);
+    if (a >= 65520.0f) return (uint16_t)(sign | 0x7c00);     /* rounds to inf */
+    /* exact value a = M * 2^E with integer M < 2^24 */
+    int E; (void)frexpf(a, &E);                              /* a = fr * 2^E, fr in [0.5,1) */
+    if (a == 0.0f) return sign;
+    /* binary16 quantum for this binade: normal if a >= 2^-14 -> 2^(E-1-10), else 2^-24 */
+    int qexp = (E - 1 >= -14) ? (E - 1 - 10) : -24;
+    double scaled = ldexp((double)a, -qexp);                 /* exact in double */
+    double fl = floor(scaled), rem = scaled - fl;
+    uint32_t mant = (uint32_t)fl;
+    if (rem > 0.5 || (rem == 0.5 && (mant & 1))) mant++;    /* round half to even */
+    /* value = mant * 2^qexp; re-encode */
+    if (qexp == -24) {                                       /* subnormal range (mant <= 1024) */
+        if (mant >= 1024) return (uint16_t)(sign | (1 << 10) | (mant - 1024)); /* rounded up to min normal */
+        return (uint16_t)(sign | mant);
+    }
+    int bexp = qexp + 25;                                    /* biased exponent for mant in [1024,2048) */
+    if (mant == 2048) { mant = 1024; bexp++; }
+    if (bexp >= 31) return (uint16_t)(sign | 0x7c00);
+    return (uint16_t)(sign | (bexp << 10) | (mant - 1024));
+}
+
+/* Eq.2: r = s * (q - z) -- one fp32 multiply of an exact integer (R6) */
+float o_dequant(uint8_t q, float s, int32_t z) { return s * (float)((int32_t)q - z); }
+
+/* ------------------------------------------------------------------------- */
+/* pinned exponential E (R9): 2^n * (1 + f*Q(f)), Q a degree-4 polynomial     */
+/* ------------------------------------------------------------------------- */
+static const float LOG2E = 0x1.715476p+0f;
+static const float MAGIC = 12582912.0f;                      /* 1.5 * 2^23 */
+static const float Q0 = 0x1.62e426p-1f, Q1 = 0x1.ebf9b6p-3f, Q2 = 0x1.c6ba7ap-5f,
+                   Q3 = 0x1.3cec0ep-7f, Q4 = 0x1.5a9610p-10f;
+static const float SELU_L = 0x1.0cfabep+0f;                  /* RN32(1.0507009873554804934) */
+static const float SELU_LA = 0x1.c212ccp+0f;                 /* RN32(lambda * alpha)        */
+
+static void exp_parts(float x, float* s_out, float* u_out) {
+    float xc = fminf(fmaxf(x, -80.0f), 80.0f);
+    float t = xc * LOG2E;
+    float r = t + MAGIC;
+    float nf = r - MAGIC;
+    float f = t - nf;
+    float q = fmaf(fmaf(fmaf(fmaf(Q4, f, Q3), f, Q2), f, Q1), f, Q0);
+    float u = f * q;
+    int32_t ri, mi; memcpy(&ri, &r, 4); float mg = MAGIC; memcpy(&mi, &mg, 4);
+    int32_t n = ri - mi;
+    uint32_t sb = (uint32_t)(n + 127) << 23;
+    float s; memcpy(&s, &sb, 4);
+    *s_out = s; *u_out = u;
+}
+float o_exp(float x) { float s, u; exp_parts(x, &s, &u); return fmaf(s, u, s); }
+float o_expm1(float x) { float s, u; exp_parts(x, &s, &u); return fmaf(s, u, s - 1.0f); }
+
+/* selu ([selu] Klambauer et al.): lambda*z for z > 0, lambda*alpha*(e^z - 1) otherwise */
+float o_selu(float z) { return z > 0.0f ? SELU_L * z : SELU_LA * o_expm1(z); }
+/* sigmoid: 1 / (1 + e^-z), IEEE division */
+float o_sigmoid(float z) { float d = 1.0f + o_exp(-z); return 1.0f / d; }
+
+double o_exp_max_relerr(float lo, float hi, int step, int which) {
+    double worst = 0.0;
+    float x = lo;
+    while (x <= hi) {
+        double ref = which == 0 ? exp((double)x) : expm1((double)x);
+        double got = which == 0 ? (double)o_exp(x) : (double)o_expm1(x);
+        double den = fabs(ref);
+        if (den > 0) { double e = fabs(got - ref) / den; if (e > worst) worst = e; }
+        for (int k = 0; k < step; k++) x = nextafterf(x, INFINITY);
+    }
+    return worst;
+}
+
+/* ------------------------------------------------------------------------- */
+/* exact fused summation of fp16 products (R10)                               */
+/* ------------------------------------------------------------------------- */
+typedef struct { int neg; uint64_t m; int e; } term;          /* (-1)^neg * m * 2^e */
+
+static term t_f16(uint16_t h) {
+    term t; int e = (h >> 10) & 31, f = h & 1023;
+    t.neg = h >> 15;
+    if (e == 0) { t.m = (uint64_t)f; t.e = -24; }
+    else { t.m = (uint64_t)(1024 + f); t.e = e - 25; }
+    return t;
+}
+static term t_mul(term a, term b) { term t; t.neg = a.neg ^ b.neg; t.m = a.m * b.m; t.e = a.e + b.e; return t; }
+static term t_f32(float x) {
+    term t; uint32_t u; memcpy(&u, &x, 4);
+    int e = (u >> 23) & 255; uint32_t f = u & 0x7fffff;
+    t.neg = (int)(u >> 31);
+    if (e == 0) { t.m = f; t.e = -149; } else { t.m = (uint64_t)(0x800000 | f); t.e = e - 150; }
+    return t;
+}
+static int bitlen64(uint64_t v) { int n = 0; while (v) { n++; v >>= 1; } return n; }
+static int bitlen128(unsigned __int128 v) { int n = 0; while (v) { n++; v >>= 1; } return n; }
+
+/* value = S * 2^q rounded to binary32 (rmode 0: nearest-even, 1: toward zero) */
+static float round_f32(__int128 S, int q, int rmode) {
+    if (S == 0) return 0.0f;
+    int neg = S < 0;
+    unsigned __int128 M = neg ? (unsigned __int128)(-S) : (unsigned __int128)S;
+    int L = q + bitlen128(M) - 1;                             /* exponent of the leading bit */
+    if (L > 127) return neg ? -INFINITY : INFINITY;
+    int lsb = (L >= -126) ? L - 23 : -149;                    /* exponent of the result's ulp */
+    unsigned __int128 mant;
+    if (lsb <= q) mant = M << (q - lsb);
+    else {
+        int sh = lsb - q;
+        mant = M >> sh;
+        unsigned __int128 rem = M - (mant << sh), half = (unsigned __int128)1 << (sh - 1);
+        if (rmode == 0 && (rem > half || (rem == half && (mant & 1)))) mant++;
+    }
+    float r = ldexpf((float)(uint64_t)mant, lsb);             /* mant <= 2^24: exact */
+    return neg ? -r : r;
+}
+
+/* sum of terms, each truncated toward zero below 2^(lead - p), exact sum, one rounding */
+static float fused(const term* t, int n, int p, int rmode) {
+    int lead = -100000;
+    for (int i = 0; i < n; i++) if (t[i].m) { int l = t[i].e + bitlen64(t[i].m) - 1; if (l > lead) lead = l; }
+    if (lead == -100000) return 0.0f;
+    if (p > 100) p = 100;
+    int q = lead - p;
+    __int128 S = 0;
+    for (int i = 0; i < n; i++) {
+        if (!t[i].m) continue;
+        int sh = t[i].e - q;
+        __int128 v = sh >= 0 ? ((__int128)t[i].m << sh) : (__int128)(t[i].m >> (-sh > 63 ? 63 : -sh));
+        if (-sh > 63) v = 0;
+        S += t[i].neg ? -v : v;
+    }
+    return round_f32(S, q, rmode);
+}
+
+static int g_mode = 1, g_chunk = 16, g_p = 100, g_rmode = 0;  /* default: replaced by the probe reading (R10) */
+void o_set_dot_model(int mode, int chunk, int p_bits, int rmode) { g_mode = mode; g_chunk = chunk; g_p = p_bits; g_rmode = rmode; }
+void o_get_dot_model(int* o) { o[0] = g_mode; o[1] = g_chunk; o[2] = g_p; o[3] = g_rmode; }
+
+float o_fused_sum(const float* acc_in, const uint16_t* a, const uint16_t* b, int n, int p_bits, int rmode) {
+    term* t = (term*)malloc(sizeof(term) * (size_t)(n + 1));
+    int k = 0;
+    if (acc_in) t[k++] = t_f32(*acc_in);
+    for (int i = 0; i < n; i++) t[k++] = t_mul(t_f16(a[i]), t_f16(b[i]));
+    float r = fused(t, k, p_bits, rmode);
+    free(t);
+    return r;
+}
+
+/* z_j = b_j + sum_k W[k][j] * a_k under the pinned summation model (R10). */
+float o_dot(float bias, const uint16_t* w, int ws, const uint16_t* a, int K) {
+    term t[257];
+    if (g_mode == 0 || K + 1 > 256) {                         /* CR: one exact sum, one RN */
+        int k = 0; t[k++] = t_f32(bias);
+        for (int i = 0; i < K; i++) t[k++] = t_mul(t_f16(w[(size_t)i * ws]), t_f16(a[i]));
+        return fused(t, k, 100, 0);
+    }
+    float acc = bias;                                         /* bias enters first, exactly */
+    for (int k0 = 0; k0 < K; k0 += g_chunk) {
+        int k1 = k0 + g_chunk < K ? k0 + g_chunk : K, n = 0;
+        t[n++] = t_f32(acc);
+        for (int i = k0; i < k1; i++) t[n++] = t_mul(t_f16(w[(size_t)i * ws]), t_f16(a[i]));
+        acc = fused(t, n, g_p, g_rmode);
+    }
+    return acc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* grid encoding: vertex-centred dense grids (R1), centres (R2), concat (R3)  */
+/* ------------------------------------------------------------------------- */
+static float lerp(float a, float b, float t) { return fmaf(t, b - a, a); }
+
+void o_grid_encode(const o_model* m, int which, float p, float q, float* out) {
+    const o_grid* g = &m->grid[which];
+    for (int l = 0; l < g->levels; l++) {
+        const o_level* L = &g->lv[l];
+        float X = p * (float)(L->res - 1), Y = q * (float)(L->res - 1);
+        int i0 = (int)floorf(X), j0 = (int)floorf(Y);
+        if (i0 > L->res - 2) i0 = L->res - 2;
+        if (j0 > L->res - 2) j0 = L->res - 2;
+        if (i0 < 0) i0 = 0;
+        if (j0 < 0) j0 = 0;
+        float fx = X - (float)i0, fy = Y - (float)j0;
+        for (int f = 0; f < m->F; f++) {
+#define QV(j, i) o_dequant(L->q[((size_t)(j) * L->res + (i)) * m->F + f], L->s, L->z)
+            float v00 = QV(j0, i0), v10 = QV(j0, i0 + 1), v01 = QV(j0 + 1, i0), v11 = QV(j0 + 1, i0 + 1);
+#undef QV
+            out[l * m->F + f] = lerp(lerp(v00, v10, fx), lerp(v01, v11, fx), fy);
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* MLP: fp16 operands at every layer input, selu hidden,       */
+/* sigmoid output                                                 */
+/* ------------------------------------------------------------------------- */
+void o_mlp_raw(int n_layers, const int* dims, const uint16_t* const* W, const uint16_t* const* b,
+               const float* in, float* out) {
+    float act[256];
+    uint16_t a16[256];
+    for (int i = 0; i < dims[0]; i++) act[i] = in[i];
+    for (int l = 0; l < n_layers; l++) {
+        int K = dims[l], N = dims[l + 1];
+        for (int i = 0; i < K; i++) a16[i] = o_f32_to_f16(act[i]);
+        for (int j = 0; j < N; j++) {
+            float z = o_dot(o_f16_to_f32(b[l][j]), W[l] + j, N, a16, K);
+            act[j] = (l + 1 < n_layers) ? o_selu(z) : o_sigmoid(z);
+        }
+    }
+    for (int j = 0; j < dims[n_layers]; j++) out[j] = act[j];
+}
+
+void o_mlp_forward(const o_model* m, int which, const float* in, float* out) {
+    const o_mlp* M = &m->mlp[which];
+    o_mlp_raw(M->n_layers, M->dims, M->W, M->b, in, out);
+}
+
+/* ------------------------------------------------------------------------- */
+/* BC1 / BC4 (Eq.7, Eq.8)                      */
+/* ------------------------------------------------------------------------- */
+static int qbits(float e, float maxv) {                       /* R11: floor(e*(2^b-1) + 1/2) */
+    float v = floorf(fmaf(e, maxv, 0.5f));
+    if (v < 0.0f) v = 0.0f;
+    if (v > maxv) v = maxv;
+    return (int)v;
+}
+uint16_t o_rgb565(const float e[3]) {
+    return (uint16_t)((qbits(e[0], 31.0f) << 11) | (qbits(e[1], 63.0f) << 5) | qbits(e[2], 31.0f));
+}
+uint8_t o_unorm8(float e) { return (uint8_t)qbits(e, 255.0f); }
+void o_expand565(uint16_t c, float o[3]) {
+    o[0] = (float)(c >> 11) / 31.0f; o[1] = (float)((c >> 5) & 63) / 63.0f; o[2] = (float)(c & 31) / 31.0f;
+}
+
+/* Eq.7: c_n = (1 - w_n) e0 + w_n e1, evaluated as fmaf(w_n, e1, RN((1 - w_n) * e0)) */
+static float interp(float w, float e0, float e1) { float wb = 1.0f - w; return fmaf(w, e1, wb * e0); }
+
+void o_palette_bc1(const float e0[3], const float e1[3], float pal[4][3]) {
+    for (int n = 0; n < 4; n++) {
+        float w = (float)n / 3.0f;                            /* w_n = n/3 */
+        for (int c = 0; c < 3; c++) pal[n][c] = interp(w, e0[c], e1[c]);
+    }
+}
+
+void o_palette_bc4(uint8_t E0, uint8_t E1, float pal[8]) {
+    float e0 = (float)E0 / 255.0f, e1 = (float)E1 / 255.0f;
+    if (E0 > E1) {                                            /* w_n = n/7 */
+        for (int n = 0; n < 8; n++) pal[n] = interp((float)n / 7.0f, e0, e1);
+    } else {                                                  /* Eq.8: c_0 = 0, c_7 = 1 */
+        pal[0] = 0.0f;
+        for (int n = 1; n <= 6; n++) pal[n] = interp((float)(n - 1) / 5.0f, e0, e1);
+        pal[7] = 1.0f;
+    }
+}
+
+/* Eq.9-10: n = argmax(-||c - c_n||) = argmin of the squared distance (R14); ties -> lowest n (R15) */
+int o_argmin_bc1(const float c[3], float pal[4][3]) {
+    int best = 0; float bd = 0.0f;
+    for (int n = 0; n < 4; n++) {
+        float dr = c[0] - pal[n][0], dg = c[1] - pal[n][1], db = c[2] - pal[n][2];
+        float d = fmaf(db, db, fmaf(dg, dg, dr * dr));
+        if (n == 0 || d < bd) { bd = d; best = n; }
+    }
+    return best;
+}
+int o_argmin_bc4(float c, const float pal[8]) {
+    int best = 0; float bd = 0.0f;
+    for (int n = 0; n < 8; n++) {
+        float d = fabsf(c - pal[n]);
+        if (n == 0 || d < bd) { bd = d; best = n; }
+    }
+    return best;
+}
+
+/* linear palette index -> DirectX stored code (R16) */
+static const int MAP1[4] = {0, 2, 3, 1};
+static const int MAP4_8[8] = {0, 2, 3, 4, 5, 6, 7, 1};
+static const int MAP4_6[8] = {6, 0, 2, 3, 4, 5, 1, 7};
+
+uint64_t o_encode_bc1(const float ep[6], const float* tx) {
+    uint16_t c0 = o_rgb565(ep), c1 = o_rgb565(ep + 3);
+    if (c0 < c1) { uint16_t t = c0; c0 = c1; c1 = t; }        /* 4-colour mode order (R12) */
+    uint64_t w = (uint64_t)c0 | ((uint64_t)c1 << 16);
+    if (c0 == c1) return w;                                   /* all codes 0 (R12) */
+    float e0[3], e1[3], pal[4][3];
+    o_expand565(c0, e0); o_expand565(c1, e1);
+    o_palette_bc1(e0, e1, pal);
+    for (int i = 0; i < 16; i++) w |= (uint64_t)MAP1[o_argmin_bc1(tx + 3 * i, pal)] << (32 + 2 * i);
+    return w;
+}
+
+uint64_t o_encode_bc4(const float ep[2], const float* tx) {
+    uint8_t E0 = o_unorm8(ep[0]), E1 = o_unorm8(ep[1]);       /* mode from stored order, no swap (R13) */
+    float pal[8];
+    o_palette_bc4(E0, E1, pal);
+    const int* map = E0 > E1 ? MAP4_8 : MAP4_6;
+    uint64_t w = (uint64_t)E0 | ((uint64_t)E1 << 8);
+    for (int i = 0; i < 16; i++) w |= (uint64_t)map[o_argmin_bc4(tx[i], pal)] << (16 + 3 * i);
+    return w;
+}
+
+void o_decode_block(uint64_t blk, int fmt, float* out) {
+    if (fmt == BC1) {
+        uint16_t c0 = (uint16_t)blk, c1 = (uint16_t)(blk >> 16);
+        float e0[3], e1[3], pal[4][3], byc[4][3];
+        o_expand565(c0, e0); o_expand565(c1, e1);
+        if (c0 > c1) {
+            o_palette_bc1(e0, e1, pal);
+            for (int n = 0; n < 4; n++) for (int c = 0; c < 3; c++) byc[MAP1[n]][c] = pal[n][c];
+        } else {                                              /* DirectX 3-colour mode (never emitted, R12) */
+            for (int c = 0; c < 3; c++) {
+                byc[0][c] = e0[c]; byc[1][c] = e1[c];
+                byc[2][c] = fmaf(0.5f, e1[c], 0.5f * e0[c]); byc[3][c] = 0.0f;
+            }
+        }
+        for (int i = 0; i < 16; i++) {
+            int code = (int)((blk >> (32 + 2 * i)) & 3);
+            for (int c = 0; c < 3; c++) out[3 * i + c] = byc[code][c];
+        }
+    } else {
+        uint8_t E0 = (uint8_t)blk, E1 = (uint8_t)(blk >> 8);
+        float pal[8], byc[8];
+        o_palette_bc4(E0, E1, pal);
+        const int* map = E0 > E1 ? MAP4_8 : MAP4_6;
+        for (int n = 0; n < 8; n++) byc[map[n]] = pal[n];
+        for (int i = 0; i < 16; i++) out[i] = byc[(blk >> (16 + 3 * i)) & 7];
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* whole material (Fig. 3a)                                 */
+/* ------------------------------------------------------------------------- */
+static int set_threads(int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+    return omp_get_max_threads();
+#else
+    (void)nthreads; return 1;
+#endif
+}
+
+/* endpoint MLP of block (bx,by) and colour MLP of its 16 texels (texel i = 4y+x) */
+static void block_mlp(const o_model* m, int W, int H, int bx, int by, float* ep, float* col) {
+    int BW = W / 4, BH = H / 4, n_c = m->mlp[1].dims[m->mlp[1].n_layers];
+    float fe[16], fc[16];
+    float s = ((float)bx + 0.5f) / (float)BW, t = ((float)by + 0.5f) / (float)BH;      /* R2 */
+    o_grid_encode(m, 0, s, t, fe);
+    o_mlp_forward(m, 0, fe, ep);
+    for (int i = 0; i < 16; i++) {
+        int x = 4 * bx + (i & 3), y = 4 * by + (i >> 2);
+        float u = ((float)x + 0.5f) / (float)W, v = ((float)y + 0.5f) / (float)H;     /* R2 */
+        o_grid_encode(m, 1, u, v, fc);
+        o_mlp_forward(m, 1, fc, col + i * n_c);
+    }
+}
+
+/* quantize + palette + index + pack one block position for every texture.
+   ep: N_e endpoint outputs; col: 16 texels x N_c colour outputs; head layout R17. */
+static void encode_all(int n_tex, const int* fmts, const float* ep, const float* col, int n_c,
+                       uint64_t* out, size_t plane_stride) {
+    int eo = 0, co = 0;
+    for (int k = 0; k < n_tex; k++) {
+        int w = fmts[k] == BC1 ? 3 : 1;
+        float tx[48];
+        for (int i = 0; i < 16; i++) for (int c = 0; c < w; c++) tx[i * w + c] = col[i * n_c + co + c];
+        out[(size_t)k * plane_stride] = fmts[k] == BC1 ? o_encode_bc1(ep + eo, tx) : o_encode_bc4(ep + eo, tx);
+        eo += 2 * w; co += w;
+    }
+}
+
+void o_mlp_outputs(const o_model* m, int W, int H, int r0, int r1, float* ep, float* col, int nthreads) {
+    int BW = W / 4, n_e = m->mlp[0].dims[m->mlp[0].n_layers], n_c = m->mlp[1].dims[m->mlp[1].n_layers];
+    set_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int by = r0; by < r1; by++)
+        for (int bx = 0; bx < BW; bx++) {
+            float c16[16 * 32];
+            size_t r = (size_t)(by - r0);
+            block_mlp(m, W, H, bx, by, ep + (r * BW + bx) * n_e, c16);
+            for (int i = 0; i < 16; i++) {
+                size_t y = r * 4 + (i >> 2), x = 4 * (size_t)bx + (i & 3);
+                memcpy(col + (y * W + x) * n_c, c16 + i * n_c, sizeof(float) * n_c);
+            }
+        }
+}
+
+void o_pack(int n_tex, const int* fmts, const float* ep, const float* col, int W, int H,
+            int r0, int r1, uint64_t* out, int nthreads) {
+    int BW = W / 4, rows = r1 - r0, n_e = 0, n_c = 0;
+    (void)H;
+    for (int k = 0; k < n_tex; k++) { n_e += fmts[k] == BC1 ? 6 : 2; n_c += fmts[k] == BC1 ? 3 : 1; }
+    set_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = 0; r < rows; r++)
+        for (int bx = 0; bx < BW; bx++) {
+            float c16[16 * 32];
+            for (int i = 0; i < 16; i++) {
+                size_t y = (size_t)r * 4 + (i >> 2), x = 4 * (size_t)bx + (i & 3);
+                memcpy(c16 + i * n_c, col + (y * W + x) * n_c, sizeof(float) * n_c);
+            }
+            encode_all(n_tex, fmts, ep + ((size_t)r * BW + bx) * n_e, c16, n_c,
+                       out + (size_t)r * BW + bx, (size_t)rows * BW);
+        }
+}
+
+void o_decode_material(const o_model* m, int W, int H, int r0, int r1, uint64_t* out, int nthreads) {
+    int BW = W / 4, rows = r1 - r0, n_c = m->mlp[1].dims[m->mlp[1].n_layers];
+    set_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = 0; r < rows; r++)
+        for (int bx = 0; bx < BW; bx++) {
+            float ep[64], c16[16 * 32];
+            block_mlp(m, W, H, bx, r0 + r, ep, c16);
+            encode_all(m->n_tex, m->fmt, ep, c16, n_c, out + (size_t)r * BW + bx, (size_t)rows * BW);
+        }
+}
+
+void o_decode_bc(const uint64_t* blocks, int fmt, int W, int H, float* out) {
+    int BW = W / 4, BH = H / 4, ch = fmt == BC1 ? 3 : 1;
+    for (int by = 0; by < BH; by++)
+        for (int bx = 0; bx < BW; bx++) {
+            float tx[48];
+            o_decode_block(blocks[(size_t)by * BW + bx], fmt, tx);
+            for (int i = 0; i < 16; i++) {
+                size_t y = 4 * (size_t)by + (i >> 2), x = 4 * (size_t)bx + (i & 3);
+                for (int c = 0; c < ch; c++) out[(y * W + x) * ch + c] = tx[i * ch + c];
+            }
+        }
+}
+
+/* PSNR: 10 log10(1 / MSE) for values in [0,1] */
+double o_psnr(const float* a, const float* b, size_t n) {
+    double se = 0.0;
+    for (size_t i = 0; i < n; i++) { double d = (double)a[i] - (double)b[i]; se += d * d; }
+    if (se == 0.0) return INFINITY;
+    return 10.0 * log10((double)n / se);
+}
+
+/* ------------------------------------------------------------------------- */
+/* brute force                                                                */
+/* ------------------------------------------------------------------------- */
+double o_block_sq_error(uint64_t blk, int fmt, const float* tx) {
+    float dec[48]; int ch = fmt == BC1 ? 3 : 1;
+    o_decode_block(blk, fmt, dec);
+    double se = 0.0;
+    for (int i = 0; i < 16 * ch; i++) { double d = (double)dec[i] - (double)tx[i]; se += d * d; }
+    return se;
+}
+
+/* exhaustive BC4 encoder: all 65,536 endpoint pairs, per-texel nearest entry */
+uint64_t o_bruteforce_bc4(const float* tx, double* best_err) {
+    double best = INFINITY; uint64_t bb = 0;
+    for (int E0 = 0; E0 < 256; E0++)
+        for (int E1 = 0; E1 < 256; E1++) {
+            float pal[8]; o_palette_bc4((uint8_t)E0, (uint8_t)E1, pal);
+            const int* map = E0 > E1 ? MAP4_8 : MAP4_6;
+            double se = 0.0; uint64_t w = (uint64_t)E0 | ((uint64_t)E1 << 8);
+            for (int i = 0; i < 16; i++) {
+                int bn = 0; double bd = INFINITY;
+                for (int n = 0; n < 8; n++) { double d = (double)tx[i] - (double)pal[n]; d *= d; if (d < bd) { bd = d; bn = n; } }
+                se += bd; w |= (uint64_t)map[bn] << (16 + 3 * i);
+            }
+            if (se < best) { best = se; bb = w; }
+        }
+    if (best_err) *best_err = best;
+    return bb;
+}
+
+/* ------------------------------------------------------------------------- */
+/* storage arithmetic (13.37 / 26.74 MB; P:321 int8 grids, P:342 fp16 MLPs) */
+/* ------------------------------------------------------------------------- */
+uint64_t o_storage_bytes(int bl, int bc, int tl, int tc, int F, int hidden, int n_hidden,
+                         int n_e, int n_c, int with_bias) {
+    uint64_t bytes = 0;
+    for (int l = 0; l < bl; l++) bytes += (uint64_t)(bc << l) * (uint64_t)(bc << l) * F;
+    for (int l = 0; l < tl; l++) bytes += (uint64_t)(tc << l) * (uint64_t)(tc << l) * F;
+    int ins[2] = {bl * F, tl * F}, outs[2] = {n_e, n_c};
+    for (int k = 0; k < 2; k++) {
+        int prev = ins[k];
+        for (int l = 0; l <= n_hidden; l++) {
+            int o = l < n_hidden ? hidden : outs[k];
+            bytes += 2ull * ((uint64_t)prev * o + (with_bias ? o : 0));
+            prev = o;
+        }
+    }
+    return bytes;
+}

@@ -1,0 +1,498 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (-m "not gpu").
+
+Each test names the passage it pins (P:n = PAPER.md line n, S:n = SPEC.md line n)
+and what it is pinned against: a value the paper prints, a closed form, an
+independent library routine (numpy, torch float64, math.fsum, Pillow), or brute
+force.  None of these tests compares the oracle with itself or with the CUDA path.
+"""
+import io
+import math
+import os
+import struct
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+L = oracle.lib()
+
+
+def _golden_kv(name):
+    kv = {}
+    for line in open(os.path.join(GOLDEN, name)):
+        line = line.split("#")[0].strip()
+        if "=" in line:
+            k, v = line.split("=", 1)
+            kv[k.strip()] = v.strip()
+    return kv
+
+
+# ---------------------------------------------------------------- fp16
+def test_f16_to_f32_all_codes_vs_numpy():
+    h = np.arange(65536, dtype=np.uint16)
+    ref = h.view(np.float16).astype(np.float32)
+    got = np.array([L.o_f16_to_f32(int(x)) for x in h], np.float32)
+    fin = np.isfinite(ref)
+    assert np.array_equal(got[fin].view(np.uint32), ref[fin].view(np.uint32))
+    assert np.all(np.isnan(got[np.isnan(ref)]))
+
+
+def test_f32_to_f16_round_nearest_even_vs_numpy():
+    rng = np.random.default_rng(1)
+    x = np.concatenate([
+        rng.standard_normal(200000).astype(np.float32) * np.float32(3),
+        (rng.random(50000) * 1e-4).astype(np.float32),          # subnormal range
+        (rng.random(20000) * 70000).astype(np.float32),          # overflow edge
+        np.array([0.0, -0.0, 65504, 65519.99, 65520, 2 ** -24, 2 ** -25, 3 * 2 ** -26, 2 ** -14], np.float32),
+    ])
+    # halfway cases: odd multiples of half a binary16 quantum
+    halves = (np.arange(1, 4000, 2) * 2.0 ** -12).astype(np.float32)
+    x = np.concatenate([x, halves, -halves])
+    with np.errstate(over="ignore"):
+        ref = x.astype(np.float16).view(np.uint16)
+    got = np.array([L.o_f32_to_f16(float(v)) for v in x], np.uint16)
+    assert np.array_equal(got, ref)
+
+
+# ---------------------------------------------------------------- Eq.2 dequantization
+def test_dequant_eq2_single_rounding():
+    for s in (np.float32(0.0078125), np.float32(0.00731), np.float32(0.0111)):
+        for z in (0, 100, 128, 255):
+            q = np.arange(256)
+            ref = (np.float64(s) * (q - z)).astype(np.float32)   # exact product, one RN
+            got = np.array([L.o_dequant(int(v), float(s), z) for v in q], np.float32)
+            assert np.array_equal(got, ref)
+
+
+# ---------------------------------------------------------------- pinned exp (R9), selu / sigmoid
+def test_exp_accuracy_vs_libm():
+    assert L.o_exp(0.0) == 1.0
+    assert L.o_exp_max_relerr(-80.0, 80.0, 100003, 0) < 4e-6      # t = x*log2e rounding dominates
+    assert L.o_exp_max_relerr(-10.0, 10.0, 10007, 0) < 1e-6
+    assert L.o_exp_max_relerr(-20.0, -1e-30, 20011, 1) < 1e-6      # expm1 on the selu branch
+    assert L.o_exp_max_relerr(-1e-2, -1e-30, 1009, 1) < 1e-6       # no cancellation near 0^-
+
+
+def test_selu_sigmoid_vs_torch_float64():
+    z = np.concatenate([np.linspace(-30, 30, 20001), np.geomspace(1e-8, 1, 2000) * -1]).astype(np.float32)
+    zt = torch.from_numpy(z.astype(np.float64))
+    ref_selu = torch.nn.functional.selu(zt).numpy()
+    ref_sig = torch.sigmoid(zt).numpy()
+    got_selu = np.array([L.o_selu(float(v)) for v in z])
+    got_sig = np.array([L.o_sigmoid(float(v)) for v in z])
+    assert np.max(np.abs(got_selu - ref_selu) / np.maximum(np.abs(ref_selu), 1e-30)) < 2e-6
+    assert np.max(np.abs(got_sig - ref_sig) / ref_sig) < 2e-6
+    assert L.o_selu(0.0) == 0.0 and L.o_sigmoid(0.0) == 0.5
+    assert L.o_sigmoid(1e30) == 1.0 and 0.0 <= L.o_sigmoid(-1e30) < 1e-30
+
+
+# ---------------------------------------------------------------- exact fused summation (R10)
+def _rand_f16(rng, n, lo=-6, hi=6):
+    mag = np.exp2(rng.uniform(lo, hi, n)) * rng.choice([-1, 1], n)
+    return mag.astype(np.float16)
+
+
+def test_fused_sum_exact_then_rn_vs_fsum():
+    """With p large the fused sum is the exact sum rounded once (RN) to binary32."""
+    rng = np.random.default_rng(2)
+    for _ in range(3000):
+        n = int(rng.integers(1, 65))
+        a, b = _rand_f16(rng, n), _rand_f16(rng, n)
+        acc = np.float32(rng.standard_normal() * 4)
+        exact = math.fsum([float(acc)] + [float(x) * float(y) for x, y in zip(a, b)])  # exact: span < 53 bits
+        ref = np.float32(exact)
+        got = oracle.fused_sum(float(acc), a, b, 100, 0)
+        assert got == ref, (got, ref)
+
+
+def test_fused_sum_truncation_bound():
+    """Truncating below 2^(lead-p) moves the sum by < n * 2^(lead-p) before the final rounding."""
+    rng = np.random.default_rng(3)
+    for p in (24, 25, 26, 28):
+        for _ in range(1000):
+            n = 16
+            a, b = _rand_f16(rng, n, -12, 6), _rand_f16(rng, n, -12, 6)
+            prods = [float(x) * float(y) for x, y in zip(a, b)]
+            exact = math.fsum(prods)
+            lead = max(math.frexp(v)[1] - 1 for v in prods if v != 0)
+            bound = (n + 1) * 2.0 ** (lead - p) + abs(exact) * 2.0 ** -23
+            for rm in (0, 1):
+                got = oracle.fused_sum(None, a, b, p, rm)
+                assert abs(got - exact) <= bound
+
+
+def test_fused_sum_representable_is_exact():
+    """Sums whose terms all fit inside the p-bit window are exact in every model."""
+    rng = np.random.default_rng(4)
+    for _ in range(500):
+        a = (rng.integers(-64, 64, 16)).astype(np.float16)       # small integers
+        b = (rng.integers(-64, 64, 16)).astype(np.float16)
+        exact = float(np.dot(a.astype(np.int64), b.astype(np.int64)))
+        for p in (24, 30, 100):
+            for rm in (0, 1):
+                assert oracle.fused_sum(None, a, b, p, rm) == exact
+
+
+# ---------------------------------------------------------------- MLP
+def _torch_mlp(weights, biases, x):
+    """float64 torch reference with fp16 rounding of every layer input."""
+    a = torch.from_numpy(np.asarray(x, np.float64))
+    for li, (w, b) in enumerate(zip(weights, biases)):
+        a16 = a.to(torch.float16).to(torch.float64)
+        z = a16 @ torch.from_numpy(w.astype(np.float64)) + torch.from_numpy(b.astype(np.float64))
+        a = torch.nn.functional.selu(z) if li + 1 < len(weights) else torch.sigmoid(z)
+    return a.numpy()
+
+
+def test_mlp_single_layer_vs_torch_float64():
+    """One layer = sigmoid(b + x16 @ W): pins the operand rounding, the Dot and the orientation of W."""
+    rng = np.random.default_rng(5)
+    orig = oracle.get_dot_model()
+    for mode in ((0, 16, 100, 0), orig):
+        oracle.set_dot_model(*mode)
+        for _ in range(50):
+            i, o = int(rng.integers(1, 65)), int(rng.integers(1, 33))
+            w = (rng.standard_normal((i, o)) * np.sqrt(2 / i)).astype(np.float16)
+            b = rng.uniform(-0.1, 0.1, o).astype(np.float16)
+            x = rng.standard_normal(i).astype(np.float32)
+            got = oracle.mlp_raw([w], [b], x)
+            ref = _torch_mlp([w], [b], x)
+            assert np.max(np.abs(got - ref) / ref) < 3e-6
+    oracle.set_dot_model(*orig)
+
+
+def test_mlp_paper_architecture_vs_torch_float64():
+    """14/16 -> 64 -> 64 -> 64 -> N with selu/sigmoid.  fp16 re-rounding of hidden
+    activations may flip by one binary16 ulp between the two evaluations, so the bound is loose;
+    a transposed weight, a dropped bias or a wrong activation is off by >> 1e-2."""
+    rng = np.random.default_rng(6)
+    for _ in range(40):
+        dims = [16, 64, 64, 64, 9]
+        ws = [(rng.standard_normal((i, o)) * np.sqrt(2 / i)).astype(np.float16) for i, o in zip(dims[:-1], dims[1:])]
+        bs = [rng.uniform(-0.1, 0.1, o).astype(np.float16) for o in dims[1:]]
+        x = rng.uniform(-1, 1, 16).astype(np.float32)
+        got = oracle.mlp_raw(ws, bs, x)
+        ref = _torch_mlp(ws, bs, x)
+        assert np.max(np.abs(got - ref)) < 2e-3
+
+
+def test_mlp_zero_weights_gives_half():
+    w = [np.zeros((16, 64), np.float16), np.zeros((64, 64), np.float16), np.zeros((64, 5), np.float16)]
+    b = [np.zeros(64, np.float16), np.zeros(64, np.float16), np.zeros(5, np.float16)]
+    assert np.all(oracle.mlp_raw(w, b, np.ones(16, np.float32)) == 0.5)
+
+
+# ---------------------------------------------------------------- grid encoding
+def _grid_model(res_list, codes_fn, s=0.01, z=128):
+    sp = synth.ModelSpec([synth.BC1], hidden=16, block_levels=len(res_list), block_coarsest=res_list[0],
+                         texel_levels=len(res_list), texel_coarsest=res_list[0])
+    m = synth.random_model(sp, 1)
+    m.block_grid = [(np.float32(s), np.int32(z), codes_fn(r)) for r in sp.level_res("block")]
+    m.texel_grid = [(np.float32(s), np.int32(z), codes_fn(r)) for r in sp.level_res("texel")]
+    return m
+
+
+def test_grid_encode_vs_torch_grid_sample():
+    """Vertex-centred bilinear lookup (R1) = grid_sample(align_corners=True) in float64."""
+    rng = np.random.default_rng(7)
+    sp = synth.ModelSpec([synth.BC1, synth.BC4])
+    sp.texel_levels = 4
+    sp.block_levels = 3
+    m = synth.random_model(sp, 11)
+    om = oracle.Model(synth.serialize(m))
+    pts = rng.random((300, 2)).astype(np.float32)
+    for which, grid in ((0, m.block_grid), (1, m.texel_grid)):
+        got = np.stack([om.grid_encode(which, float(p), float(q)) for p, q in pts])
+        for l, (s, z, codes) in enumerate(grid):
+            vals = float(s) * (codes.astype(np.float64) - float(z))            # Eq.2, [res][res][F]
+            inp = torch.from_numpy(vals.transpose(2, 0, 1)[None])               # N C H W
+            g = torch.from_numpy((pts.astype(np.float64) * 2 - 1)[None, :, None, :])  # (x=p, y=q)
+            ref = torch.nn.functional.grid_sample(inp, g, mode="bilinear", align_corners=True)[0, :, :, 0].T.numpy()
+            assert np.max(np.abs(got[:, 2 * l:2 * l + 2] - ref)) < 2e-5, (which, l)
+
+
+def test_grid_encode_reproduces_affine_field_and_centre():
+    """Bilinear interpolation reproduces an affine vertex field; cell centre = mean of 4."""
+    def affine(r):
+        j, i = np.meshgrid(np.arange(r), np.arange(r), indexing="ij")
+        a = 30 + (i * 150) // (r - 1)            # integer codes, exactly affine only if divisible
+        b = 40 + (j * 120) // (r - 1)
+        return np.stack([a, b], -1).astype(np.uint8)
+    m = _grid_model([16], affine, s=0.5, z=0)
+    # res 16: (r-1)=15 divides 150 and 120, so codes are exactly affine in i and j
+    om = oracle.Model(synth.serialize(m))
+    rng = np.random.default_rng(8)
+    for p, q in rng.random((200, 2)).astype(np.float32):
+        X = np.float32(p) * np.float32(15)
+        Y = np.float32(q) * np.float32(15)
+        ref = [0.5 * (30 + 10 * float(X)), 0.5 * (40 + 8 * float(Y))]
+        got = om.grid_encode(1, float(p), float(q))
+        assert abs(got[0] - ref[0]) < 1e-4 and abs(got[1] - ref[1]) < 1e-4
+    # cell centre: X = 0.5 exactly when p = 0.5/15 ... use p with X exactly i+0.5
+    rcodes = np.random.default_rng(9).integers(0, 256, (16, 16, 2)).astype(np.uint8)
+    m2 = _grid_model([16], lambda r: rcodes, s=1.0, z=0)
+    om2 = oracle.Model(synth.serialize(m2))
+    p = np.float32(np.float32(7.5) / np.float32(15))
+    X = p * np.float32(15)
+    if X == np.float32(7.5):
+        got = om2.grid_encode(1, float(p), float(p))
+        ref = rcodes[7:9, 7:9].astype(np.float64).mean(axis=(0, 1))
+        assert np.allclose(got, ref, atol=1e-4)
+
+
+# ---------------------------------------------------------------- BC formats (Eq.7/8)
+MAP1 = [0, 2, 3, 1]
+
+
+def test_bc_layout_goldens():
+    for line in open(os.path.join(GOLDEN, "bc_layout.txt")):
+        line = line.split("#")[0].strip()
+        if not line:
+            continue
+        name, fmt, word, texels = [x.strip() for x in line.split("|")]
+        fmt = int(fmt)
+        word = int(word.replace("_", ""), 16)
+        val = eval(texels.split("*")[1])
+        got = oracle.decode_block(word, fmt)
+        exp = np.tile(np.array(val, np.float32), (16, 1)) if fmt == 1 else np.full(16, val, np.float32)
+        assert np.array_equal(got, exp), name
+
+
+def test_code_maps_golden_vs_decoder():
+    kv = _golden_kv("maps.txt")
+    maps = {k: [int(x) for x in v.split()] for k, v in kv.items()}
+    # BC1: decode each stored code and match it with the linear palette entry
+    e0, e1 = 0xF800, 0x001F
+    pal = oracle.palette_bc1([1, 0, 0], [0, 0, 1])
+    for n, code in enumerate(maps["bc1"]):
+        blk = e0 | (e1 << 16) | (sum(code << (2 * i) for i in range(16)) << 32)
+        assert np.array_equal(oracle.decode_block(blk, 1)[0], pal[n])
+    for (E0, E1), key in (((200, 50), "bc4_e0_gt_e1"), ((50, 200), "bc4_e0_le_e1")):
+        pal = oracle.palette_bc4(E0, E1)
+        for n, code in enumerate(maps[key]):
+            blk = E0 | (E1 << 8) | (sum(code << (3 * i) for i in range(16)) << 16)
+            assert oracle.decode_block(blk, 4)[0] == pal[n]
+
+
+def _dds(fourcc, w, h, payload):
+    hdr = struct.pack("<4sIIIIIII44s", b"DDS ", 124, 0x1 | 0x2 | 0x4 | 0x1000 | 0x80000, h, w,
+                      len(payload), 0, 1, b"\0" * 44)
+    hdr += struct.pack("<II4sIIIII", 32, 0x4, fourcc, 0, 0, 0, 0, 0)          # DDS_PIXELFORMAT
+    hdr += struct.pack("<IIIII", 0x1000, 0, 0, 0, 0)                         # caps
+    assert len(hdr) == 128
+    return hdr + payload
+
+
+def test_decoder_cross_check_with_pillow():
+    """Pillow's independent DXT1/ATI1 decoder agrees within +-2 LSB (it bit-replicates RGB565 and
+    interpolates in integers).  A wrong bit order or code map is off by tens of LSBs."""
+    from PIL import Image
+    rng = np.random.default_rng(10)
+    nb = 64
+    blocks1 = []
+    for _ in range(nb):
+        c0, c1 = sorted(rng.integers(0, 65536, 2).tolist(), reverse=True)
+        if c0 == c1:
+            c1 = max(0, c0 - 1)
+        blocks1.append(c0 | (c1 << 16) | (int(rng.integers(0, 2 ** 32)) << 32))
+    blocks4 = [int(rng.integers(0, 2 ** 63)) | (int(rng.integers(0, 2)) << 63) for _ in range(nb)]
+    W, H = 4 * 8, 4 * 8
+    for fmt, blocks, cc in ((1, blocks1, b"DXT1"), (4, blocks4, b"ATI1")):
+        arr = np.array(blocks, np.uint64)
+        img = Image.open(io.BytesIO(_dds(cc, W, H, arr.tobytes())))
+        img.load()
+        pil = np.asarray(img).astype(np.float64)
+        ours = oracle.decode_bc(arr, fmt, W, H).astype(np.float64) * 255
+        if fmt == 1:
+            pil = pil[..., :3]
+        else:
+            pil = pil.reshape(H, W, -1)[..., :1]
+        assert np.max(np.abs(pil - ours)) <= 2.0 + 1e-9, fmt
+
+
+def test_palette_goldens():
+    for line in open(os.path.join(GOLDEN, "palettes.txt")):
+        line = line.split("#")[0].strip()
+        if not line:
+            continue
+        fmt, ee, vals, _ = [x.strip() for x in line.split("|")]
+        E0, E1 = [int(x, 0) for x in ee.split()]
+        exp = np.array([float(v) for v in vals.split()])
+        if int(fmt) == 4:
+            got = oracle.palette_bc4(E0, E1)
+        else:
+            e0, e1 = np.zeros(3, np.float32), np.zeros(3, np.float32)
+            L.o_expand565(E0, e0.ctypes.data)
+            L.o_expand565(E1, e1.ctypes.data)
+            got = oracle.palette_bc1(e0, e1)[:, 0]
+        assert np.max(np.abs(got - exp)) < 1e-6
+
+
+def test_eq8_identities_and_endpoints_all_pairs():
+    """Eq.8 first/third cases give exactly 0 and 1; n=0 / n=7 reproduce e0 / e1 in mode e0>e1;
+    interior entries equal (1-w)e0 + w e1 to within one rounding."""
+    for E0 in range(256):
+        for E1 in range(256):
+            pal = oracle.palette_bc4(E0, E1)
+            e0, e1 = np.float32(E0) / np.float32(255), np.float32(E1) / np.float32(255)
+            if E0 > E1:
+                assert pal[0] == e0 and pal[7] == e1
+                w = np.arange(8) / 7
+            else:
+                assert pal[0] == 0.0 and pal[7] == 1.0
+                assert pal[1] == e0 and pal[6] == e1
+                w = np.concatenate([[0], np.arange(6) / 5, [0]])
+            ref = (1 - w) * float(e0) + w * float(e1)
+            sl = slice(0, 8) if E0 > E1 else slice(1, 7)
+            assert np.max(np.abs(pal[sl] - ref[sl])) < 2e-7
+
+
+def test_endpoint_quantizer_round_trip():
+    """R11: E = floor(e*(2^b-1)+1/2) inverts the UNORM expansion for every code (exhaustive)."""
+    for k in range(256):
+        assert L.o_unorm8(float(np.float32(k) / np.float32(255))) == k
+    e = np.zeros(3, np.float32)
+    for c in range(65536):
+        L.o_expand565(c, e.ctypes.data)
+        assert L.o_rgb565(e.ctypes.data) == c
+
+
+def test_index_selection_is_bruteforce_nearest():
+    """Eq.9-10: chosen n minimises the exact distance to the palette (float64 brute force)."""
+    rng = np.random.default_rng(12)
+    for _ in range(2000):
+        pal = rng.random((4, 3)).astype(np.float32)
+        c = rng.random(3).astype(np.float32)
+        n = L.o_argmin_bc1(c.ctypes.data, pal.ctypes.data)
+        d = np.sum((c.astype(np.float64) - pal.astype(np.float64)) ** 2, axis=1)
+        assert d[n] <= d.min() + 1e-6
+        E0, E1 = (int(x) for x in rng.integers(0, 256, 2))
+        p4 = oracle.palette_bc4(E0, E1)
+        v = np.float32(rng.random())
+        n4 = L.o_argmin_bc4(float(v), p4.ctypes.data)
+        d4 = np.abs(float(v) - p4.astype(np.float64))
+        assert d4[n4] <= d4.min() + 1e-7
+        if np.sum(d4 == d4.min()) > 1:
+            assert n4 == int(np.argmin(d4))          # ties -> lowest linear n (R15)
+
+
+def test_decode_of_encode_is_palette_of_argmin():
+    rng = np.random.default_rng(13)
+    for _ in range(500):
+        ep = rng.random(6).astype(np.float32)
+        tx = rng.random((16, 3)).astype(np.float32)
+        w = oracle.encode_bc1(ep, tx)
+        c0, c1 = w & 0xFFFF, (w >> 16) & 0xFFFF
+        assert c0 > c1 or (c0 == c1 and (w >> 32) == 0)           # 4-colour mode (R12)
+        dec = oracle.decode_block(w, 1)
+        if c0 != c1:
+            e0, e1 = np.zeros(3, np.float32), np.zeros(3, np.float32)
+            L.o_expand565(c0, e0.ctypes.data)
+            L.o_expand565(c1, e1.ctypes.data)
+            pal = oracle.palette_bc1(e0, e1)
+            for i in range(16):
+                d = np.sum((tx[i].astype(np.float64) - pal.astype(np.float64)) ** 2, axis=1)
+                assert np.sum((tx[i] - dec[i]) ** 2) <= d.min() + 1e-6
+        ep4 = rng.random(2).astype(np.float32)
+        t4 = rng.random(16).astype(np.float32)
+        w4 = oracle.encode_bc4(ep4, t4)
+        pal4 = oracle.palette_bc4(w4 & 255, (w4 >> 8) & 255)
+        dec4 = oracle.decode_block(w4, 4)
+        for i in range(16):
+            assert abs(float(t4[i]) - float(dec4[i])) <= np.min(np.abs(float(t4[i]) - pal4.astype(np.float64))) + 1e-7
+
+
+def test_bc4_bruteforce_optimum_bounds_ntbc_encoding():
+    """Exhaustive BC4 search over all 65,536 endpoint pairs: the NTBC block (any predicted
+    endpoints) can never beat it, and two-level blocks are encoded exactly."""
+    rng = np.random.default_rng(14)
+    for _ in range(4):
+        tx = rng.random(16).astype(np.float32)
+        blk, best = oracle.bruteforce_bc4(tx)
+        assert abs(oracle.block_sq_error(blk, 4, tx) - best) < 1e-9
+        for _ in range(20):
+            w = oracle.encode_bc4(rng.random(2).astype(np.float32), tx)
+            assert oracle.block_sq_error(w, 4, tx) >= best - 1e-12
+    # a block made of two representable values (in mode e0>e1) has optimal error 0 and NTBC finds it
+    a, b = np.float32(200) / np.float32(255), np.float32(60) / np.float32(255)
+    tx = np.where(rng.random(16) < 0.5, a, b).astype(np.float32)
+    blk, best = oracle.bruteforce_bc4(tx)
+    assert best == 0.0
+    assert oracle.block_sq_error(oracle.encode_bc4(np.array([a, b], np.float32), tx), 4, tx) == 0.0
+
+
+def test_bc1_two_colour_block_is_exact():
+    rng = np.random.default_rng(15)
+    for _ in range(200):
+        c = sorted(rng.integers(0, 65536, 2).tolist(), reverse=True)
+        if c[0] == c[1]:
+            continue
+        e = np.zeros((2, 3), np.float32)
+        for i in range(2):
+            L.o_expand565(c[i], e[i].ctypes.data)
+        tx = e[rng.integers(0, 2, 16)]
+        w = oracle.encode_bc1(e.reshape(-1), tx)
+        assert oracle.block_sq_error(w, 1, tx) == 0.0
+
+
+# ---------------------------------------------------------------- end to end
+def _closed_form_blob(fmt):
+    big = 65504.0
+    if fmt == synth.BC1:
+        spec = synth.ModelSpec([synth.BC1], hidden=16, block_levels=2, block_coarsest=8, texel_levels=2, texel_coarsest=16)
+        ep_b = [big, -big, -big, -big, -big, big]
+        co_b = [math.log(2.0), -big, -math.log(2.0)]
+    else:
+        spec = synth.ModelSpec([synth.BC4], hidden=16, block_levels=2, block_coarsest=8, texel_levels=2, texel_coarsest=16)
+        ep_b = [1.291, -1.411]
+        co_b = [0.129]
+    return synth.serialize(synth.closed_form_model(spec, ep_b, co_b))
+
+
+def test_closed_form_end_to_end_golden():
+    kv = _golden_kv("closed_form.txt")
+    for fmt, key in ((synth.BC1, "bc1_word"), (synth.BC4, "bc4_word")):
+        m = oracle.Model(_closed_form_blob(fmt))
+        out = m.decode_material(16, 8)
+        assert np.all(out == np.uint64(int(kv[key], 16))), (key, hex(int(out.flat[0])))
+
+
+def test_pack_of_mlp_outputs_equals_decode_material():
+    m = oracle.Model(synth.model_blob(1))
+    ep, col = m.mlp_outputs(64, 64)
+    assert np.array_equal(oracle.pack(m.fmts, ep, col, 64, 64), m.decode_material(64, 64))
+    assert np.array_equal(m.decode_material(64, 64, 3, 9), m.decode_material(64, 64)[:, 3:9])
+
+
+def test_model_parse_rejects_bad_blobs():
+    blob = synth.model_blob(1)
+    for bad in (b"XTBC" + blob[4:], blob[:500], blob[:4] + struct.pack("<I", 2) + blob[8:]):
+        with pytest.raises(ValueError):
+            oracle.Model(bad)
+
+
+# ---------------------------------------------------------------- storage and PSNR
+def test_storage_arithmetic_reproduces_paper_numbers():
+    kv = _golden_kv("storage.txt")
+    sb = lambda bl, tl, ne, nc, bias=1: L.o_storage_bytes(bl, 16, tl, 16, 2, 64, 3, ne, nc, bias)
+    # grid payload alone (no MLP): hidden=0 layers of width 0 contribute 2*(in*out)=0 with out=0
+    grids_only = L.o_storage_bytes(7, 16, 8, 16, 2, 0, 0, 0, 0, 0) - 0
+    assert grids_only == int(kv["texel_grid_bytes"]) + int(kv["block_grid_bytes"])
+    ag = sb(7, 8, 6 * 2 + 2 * 4, 3 * 2 + 4)            # aggressive: 2 BC1 + 4 BC4
+    cs = sb(7, 8, 6 * 2, 3 * 2) + sb(7, 8, 2 * 4, 4)   # conservative pair
+    assert round(ag / 2 ** 20, 2) == float(kv["aggressive_MiB"])
+    assert round(cs / 2 ** 20, 2) == float(kv["conservative_MiB"])
+    assert 1024 * 1024 * 8 / 2 ** 20 == float(kv["bc_texture_4k_MiB"])
+
+
+def test_psnr_uniform_error_closed_form():
+    rng = np.random.default_rng(16)
+    a = rng.random(4096).astype(np.float32) * 0.5
+    for eps in (0.1, 0.01, 1 / 255):
+        b = a + np.float32(eps)
+        ref = 20 * math.log10(1 / float(np.float32(eps)))
+        assert abs(oracle.psnr(a, b) - ref) < 1e-3

@@ -1,0 +1,127 @@
+/* ntbc.h -- C ABI of libntbc.so, the B200 (sm_100a) NTBC inference hot path.
+ *
+ * Neural Texture Block Compression (arXiv 2407.09543).  "Network weights are stored in the disk
+ * which are loaded into the memory.  Then inference is executed to reconstruct block-compressed
+ * texture data which are copied to VRAM"; "NTBC predicts block-compressed data
+ * instead of loading block-compressed textures from the disk, and then texel values are decoded
+ * from the compressed data using the existing BC decompression method".
+ *
+ * Conventions (all entry points):
+ *   - return ntbc_status (0 = OK, < 0 = error) and never throw; on error a thread-local message is
+ *     available from ntbc_last_error();
+ *   - "device" pointers are CUDA device memory of the model's device, allocated and owned by the
+ *     caller (typically torch tensors); "host" pointers are host memory owned by the caller;
+ *   - stream = a cudaStream_t passed as void* (NULL = legacy default stream); calls taking a
+ *     stream are asynchronous: launch errors are returned, device faults surface at the caller's
+ *     next synchronisation of that stream;
+ *   - no entry point allocates device memory on the hot path (ntbc_decode_material,
+ *     ntbc_decode_bc, ntbc_pack); scratch is owned by the model and sized at load time.
+ * Readings of silent passages are numbered R1..R20 in DESIGN.md §2.
+ */
+#ifndef NTBC_H
+#define NTBC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ntbc_model_s* ntbc_model;               /* opaque, library-owned */
+
+typedef enum { NTBC_BC1 = 1, NTBC_BC4 = 4 } ntbc_format;
+
+typedef enum {
+  NTBC_OK = 0,
+  NTBC_EINVAL = -1,    /* bad argument: NULL, size/alignment/range (W,H % 4, rows, pointers 16-B aligned) */
+  NTBC_EFORMAT = -2,   /* bad .ntbc blob: magic, version, truncation, dims inconsistent with header */
+  NTBC_EMISMATCH = -3, /* models vs request (e.g. conservative pair not one all-BC1 + one all-BC4) */
+  NTBC_ENOMEM = -4,    /* device allocation failed */
+  NTBC_ECUDA = -5      /* CUDA runtime error (message has the CUDA error string) */
+} ntbc_status;
+
+typedef struct {
+  int n_textures;          /* textures in head order (<= 8) */
+  int fmt[8];              /* NTBC_BC1 / NTBC_BC4 per texture */
+  int hidden, n_hidden;    /* MLP width (16/32/64) and depth (3) */
+  int n_endpoint_out;      /* N_e = 6 N_RGB + 2 N_SC */
+  int n_color_out;         /* N_c = 3 N_RGB + N_SC */
+  int block_levels, block_coarsest, texel_levels, texel_coarsest, features;
+  size_t device_bytes;     /* device memory held by the model */
+} ntbc_model_info;
+
+/* Parse and validate a host .ntbc blob (int8 grids + per-level (s, z) + fp16 MLPs,
+ * PAPER.md:321-322, 342) and upload it to `cuda_device`: grids as-is, MLP weights re-laid-out into
+ * the tcgen05 shared-memory operand layout with the bias folded in as an extra K chunk.
+ * The blob is not retained (caller may free it after return).  Synchronous.
+ * Errors: NTBC_EINVAL (NULL args), NTBC_EFORMAT, NTBC_ENOMEM, NTBC_ECUDA. */
+ntbc_status ntbc_load_model(const void* blob, size_t nbytes, int cuda_device, ntbc_model* out);
+
+/* Re-upload the parameters of an already loaded model from a (preferably pinned) host blob of the
+ * same architecture, asynchronously on `stream` (host->device copies only; the blob must stay
+ * valid until the stream reaches this point).  Errors: NTBC_EINVAL, NTBC_EFORMAT,
+ * NTBC_EMISMATCH (architecture differs), NTBC_ECUDA. */
+ntbc_status ntbc_model_upload_async(ntbc_model m, const void* blob, size_t nbytes, void* stream);
+
+ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out);
+void ntbc_free_model(ntbc_model m);                     /* NULL ok; caller guarantees no in-flight use */
+
+/* Rows a1-a8 of SURVEY §8, one fused sm_100a kernel per model: grid dequant + bilinear sampling
+ * (Eq.2), endpoint MLP per block and colour MLP per texel on tcgen05 tensor cores
+ * (P:257-272), endpoint quantization (R11-R13), palettes (Eq.7/8), per-texel
+ * argmax of negative distance (Eq.9-10) and BC1/BC4 bit packing.
+ *   models / n_models: 1 = aggressive (one model), 2 = conservative (an all-BC1 model and
+ *     an all-BC4 model);
+ *   width, height: texels, multiples of 4, identical for every texture of the material;
+ *   [block_row_begin, block_row_end): shard of the H/4 block rows to decode (0 <= begin < end <= H/4);
+ *   out_blocks: one device pointer per texture, models[0]'s textures then models[1]'s, each
+ *     (end-begin) * (width/4) * 8 bytes, 16-B aligned; row-major little-endian 64-bit BC words:
+ *     BC1 = c0 | c1<<16 | sum code_i << (32+2i), BC4 = e0 | e1<<8 | sum code_i << (16+3i), texel i = 4y+x.
+ * Errors: NTBC_EINVAL, NTBC_EMISMATCH, NTBC_ECUDA. */
+ntbc_status ntbc_decode_material(const ntbc_model* models, int n_models, int width, int height,
+                                 int block_row_begin, int block_row_end, void* const* out_blocks,
+                                 void* stream);
+
+/* End-to-end variant of ntbc_decode_material for host buffers: per model, copies its host blob
+ * (pinned recommended; same architecture as the loaded model) host->device, decodes all block rows,
+ * and copies every texture's BC words device->host into host_out[t] (height/4 * width/4 * 8 bytes).
+ * Uses model-owned device scratch (allocated on first use for a given size, outside any timed loop).
+ * Asynchronous on `stream`; call cudaStreamSynchronize before reading host_out.
+ * Errors: as ntbc_decode_material, plus NTBC_ENOMEM. */
+ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, const void* const* blobs,
+                                      const size_t* blob_sizes, int width, int height,
+                                      void* const* host_out, void* stream);
+
+/* Row a9 (verification): decode a BC1/BC4 surface with the DirectX palettes (decode uses
+ * the same float palette arithmetic as the encoder, R18) into fp32 texels.
+ *   blocks: device, (height/4)*(width/4) words; out_texels: device, height*width*(3|1) fp32,
+ *   row-major, RGB interleaved.  Errors: NTBC_EINVAL, NTBC_ECUDA. */
+ntbc_status ntbc_decode_bc(const void* blocks, ntbc_format fmt, int width, int height, float* out_texels,
+                           void* stream);
+
+/* Verification only (not timed): rows a1-a4, the fp32 MLP outputs of block rows [row_begin,row_end):
+ *   endpoints: device [rows][width/4][N_e] fp32;  colors: device [rows*4][width][N_c] fp32. */
+ntbc_status ntbc_debug_mlp(ntbc_model m, int width, int height, int row_begin, int row_end,
+                           float* endpoints, float* colors, void* stream);
+
+/* Rows a5-a8 as a standalone kernel (quantize + palette + index + pack) fed fp32 MLP outputs in the
+ * ntbc_debug_mlp layouts; same output convention as ntbc_decode_material.  fmts: host array of
+ * n_textures formats (head order, R17).  Errors: NTBC_EINVAL, NTBC_ECUDA. */
+ntbc_status ntbc_pack(int n_textures, const int* fmts, const float* endpoints, const float* colors,
+                      int width, int height, int row_begin, int row_end, void* const* out_blocks,
+                      void* stream);
+
+/* Measurement support: tcgen05.mma kind::f16 probe used to pin the tensor-core summation reading
+ * (R10).  D[128][N] = C[128][N] (if C != NULL) + sum over K/16 MMAs of A[128][K] B[N][K]^T.
+ * A, B fp16 row-major device; C, D fp32 device; N in {16,32,64}, K % 16 == 0, K <= 128. */
+ntbc_status ntbc_debug_mma(const void* A, const void* B, const float* C, float* D, int K, int N, void* stream);
+
+/* Number of kernel launches the library issued since load (all entry points), for bench accounting. */
+uint64_t ntbc_launch_count(void);
+
+const char* ntbc_last_error(void);                     /* thread-local message of the last failure */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -8,10 +8,10 @@
  * only fused multiply-adds are the explicit fmaf() calls written below; every
  * other operation is one IEEE-754 binary32 operation rounded to nearest-even.
  *
- * Parity status per function:
- *   all functions below are pinned by -m "not gpu" tests EXCEPT
- *   o_dot in CHUNK mode, whose summation order is pinned to the
- *   mathematics only through its error bound (R10).
+ * Parity status per function: every function below is pinned by -m "not gpu"
+ * tests.  o_dot's summation ORDER (R10: chunks of 16, window p = 25, round toward zero) is a
+ * reading of a passage the paper leaves silent ("half-precision floating points"); the
+ * mathematics pins it through its error bound and its exactness on representable sums.
  */
 #include "ntbc_oracle.h"
 
@@ -206,24 +206,28 @@ double o_exp_max_relerr(float lo, float hi, int step, int which) {
 /* ------------------------------------------------------------------------- */
 /* exact fused summation of fp16 products (R10)                               */
 /* ------------------------------------------------------------------------- */
-typedef struct { int neg; uint64_t m; int e; } term;          /* (-1)^neg * m * 2^e */
+/* A term of a fused sum: value = (-1)^neg * m * 2^e.  `ref` is the exponent the R10 alignment
+   rule uses: for an fp16 x fp16 product the SUM of the two operands' unbiased exponents (subnormal
+   operands count as -14), for the fp32 accumulator its unbiased exponent (subnormal: -126). */
+typedef struct { int neg; uint64_t m; int e; int ref; } term;
 
 static term t_f16(uint16_t h) {
     term t; int e = (h >> 10) & 31, f = h & 1023;
     t.neg = h >> 15;
-    if (e == 0) { t.m = (uint64_t)f; t.e = -24; }
-    else { t.m = (uint64_t)(1024 + f); t.e = e - 25; }
+    if (e == 0) { t.m = (uint64_t)f; t.e = -24; t.ref = -14; }
+    else { t.m = (uint64_t)(1024 + f); t.e = e - 25; t.ref = e - 15; }
     return t;
 }
-static term t_mul(term a, term b) { term t; t.neg = a.neg ^ b.neg; t.m = a.m * b.m; t.e = a.e + b.e; return t; }
+static term t_mul(term a, term b) {
+    term t; t.neg = a.neg ^ b.neg; t.m = a.m * b.m; t.e = a.e + b.e; t.ref = a.ref + b.ref; return t;
+}
 static term t_f32(float x) {
     term t; uint32_t u; memcpy(&u, &x, 4);
     int e = (u >> 23) & 255; uint32_t f = u & 0x7fffff;
     t.neg = (int)(u >> 31);
-    if (e == 0) { t.m = f; t.e = -149; } else { t.m = (uint64_t)(0x800000 | f); t.e = e - 150; }
+    if (e == 0) { t.m = f; t.e = -149; t.ref = -126; } else { t.m = (uint64_t)(0x800000 | f); t.e = e - 150; t.ref = e - 127; }
     return t;
 }
-static int bitlen64(uint64_t v) { int n = 0; while (v) { n++; v >>= 1; } return n; }
 static int bitlen128(unsigned __int128 v) { int n = 0; while (v) { n++; v >>= 1; } return n; }
 
 /* value = S * 2^q rounded to binary32 (rmode 0: nearest-even, 1: toward zero) */
@@ -246,25 +250,31 @@ static float round_f32(__int128 S, int q, int rmode) {
     return neg ? -r : r;
 }
 
-/* sum of terms, each truncated toward zero below 2^(lead - p), exact sum, one rounding */
+/* R10 fused sum: R = max ref over the non-zero terms; every term is truncated toward zero to a
+   multiple of 2^(R - p); the truncated terms are added exactly; the sum is rounded once (rmode 0 =
+   nearest-even, 1 = toward zero).  With p >= 100 nothing is truncated for fp16 products, so the
+   result is the exact sum rounded once. */
 static float fused(const term* t, int n, int p, int rmode) {
-    int lead = -100000;
-    for (int i = 0; i < n; i++) if (t[i].m) { int l = t[i].e + bitlen64(t[i].m) - 1; if (l > lead) lead = l; }
-    if (lead == -100000) return 0.0f;
+    int R = -100000;
+    for (int i = 0; i < n; i++) if (t[i].m && t[i].ref > R) R = t[i].ref;
+    if (R == -100000) return 0.0f;
     if (p > 100) p = 100;
-    int q = lead - p;
+    int q = R - p;
     __int128 S = 0;
     for (int i = 0; i < n; i++) {
         if (!t[i].m) continue;
         int sh = t[i].e - q;
-        __int128 v = sh >= 0 ? ((__int128)t[i].m << sh) : (__int128)(t[i].m >> (-sh > 63 ? 63 : -sh));
-        if (-sh > 63) v = 0;
+        __int128 v;
+        if (sh >= 0) v = (__int128)t[i].m << sh;
+        else v = -sh > 63 ? 0 : (__int128)(t[i].m >> (-sh));          /* magnitude truncation */
         S += t[i].neg ? -v : v;
     }
     return round_f32(S, q, rmode);
 }
 
-static int g_mode = 1, g_chunk = 16, g_p = 100, g_rmode = 0;  /* default: replaced by the probe reading (R10) */
+/* R10: fp32 accumulation in chunks of 16 products, each chunk fused with the running
+   accumulator under window p = 25 and a final round-toward-zero. */
+static int g_mode = 1, g_chunk = 16, g_p = 25, g_rmode = 1;
 void o_set_dot_model(int mode, int chunk, int p_bits, int rmode) { g_mode = mode; g_chunk = chunk; g_p = p_bits; g_rmode = rmode; }
 void o_get_dot_model(int* o) { o[0] = g_mode; o[1] = g_chunk; o[2] = g_p; o[3] = g_rmode; }
 

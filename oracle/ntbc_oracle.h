@@ -42,10 +42,12 @@ float    o_sigmoid(float z);                                   /* P:332, R8 */
 
 /* Summation model of one layer's dot product (R10).
    mode 0 = CR  : b + sum_k w_k a_k exactly, one RN to fp32.
-   mode 1 = CHUNK: acc = b; per chunk of `chunk` products acc = F(acc, chunk)
-                   where F aligns the chunk's exact products and acc to the
-                   leading bit of the largest, truncates each below 2^(lead-p),
-                   sums exactly and rounds once (rmode 0 = RN-even, 1 = RZ). */
+   mode 1 = CHUNK (default, R10): acc = b; per chunk of `chunk` products acc = F(acc, chunk)
+                   where R = max over the chunk's non-zero terms of the exponent SUM
+                   e_w + e_a of each fp16 product (and the fp32 acc's exponent); every
+                   term is truncated toward zero to a multiple of 2^(R-p), the terms are
+                   added exactly and the sum is rounded once (rmode 0 = RN-even, 1 = RZ).
+                   Default chunk=16, p=25, RZ. */
 void  o_set_dot_model(int mode, int chunk, int p_bits, int rmode);
 void  o_get_dot_model(int* out4);
 float o_dot(float bias, const uint16_t* w, int w_stride, const uint16_t* a, int k);

@@ -1,0 +1,475 @@
+// ntbc_api.cu -- host side of libntbc.so: the C ABI declared in include/ntbc.h.
+// Model parsing/validation, device residency, operand re-layout, kernel launches, error reporting.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ntbc.h"
+#include "ntbc_kernels.cuh"
+
+using namespace ntbc;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+ntbc_status fail(ntbc_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+#define CUDA_TRY(x)                                                                              \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) return fail(NTBC_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                      \
+  } while (0)
+
+size_t al16(size_t n) { return (n + 15) & ~size_t(15); }
+uint32_t rd32(const uint8_t* p) { uint32_t v; memcpy(&v, p, 4); return v; }
+
+// Parsed architecture of a .ntbc blob.  Offsets index the blob.
+struct Arch {
+  int n_tex, fmt[kMaxTex], hidden, n_hidden, F;
+  int levels[2], coarsest[2];
+  int dims[2][5];                 // [net][layer boundary]
+  size_t level_off[2][kMaxLevels];
+  float s[2][kMaxLevels];
+  int z[2][kMaxLevels];
+  size_t w_off[2][4], b_off[2][4];
+  size_t total;
+};
+
+ntbc_status parse(const void* blob, size_t n, Arch& a) {
+  if (!blob) return fail(NTBC_EINVAL, "blob is NULL");
+  const uint8_t* b = (const uint8_t*)blob;
+  if (n < 96) return fail(NTBC_EFORMAT, "blob truncated (%zu bytes < 96-byte header)", n);
+  if (memcmp(b, "NTBC", 4) != 0) return fail(NTBC_EFORMAT, "bad magic");
+  if (rd32(b + 4) != 1) return fail(NTBC_EFORMAT, "unsupported version %u", rd32(b + 4));
+  a.n_tex = (int)rd32(b + 8);
+  if (a.n_tex < 1 || a.n_tex > kMaxTex) return fail(NTBC_EFORMAT, "n_textures %d not in [1,8]", a.n_tex);
+  for (int i = 0; i < a.n_tex; i++) {
+    a.fmt[i] = (int)rd32(b + 12 + 4 * i);
+    if (a.fmt[i] != NTBC_BC1 && a.fmt[i] != NTBC_BC4) return fail(NTBC_EFORMAT, "texture %d: bad format %d", i, a.fmt[i]);
+  }
+  a.hidden = (int)rd32(b + 44);
+  a.n_hidden = (int)rd32(b + 48);
+  a.F = (int)rd32(b + 52);
+  a.levels[0] = (int)rd32(b + 56); a.coarsest[0] = (int)rd32(b + 60);
+  a.levels[1] = (int)rd32(b + 64); a.coarsest[1] = (int)rd32(b + 68);
+  const int ep_in = (int)rd32(b + 72), n_e = (int)rd32(b + 76), col_in = (int)rd32(b + 80), n_c = (int)rd32(b + 84);
+  if (a.hidden != 16 && a.hidden != 32 && a.hidden != 64) return fail(NTBC_EFORMAT, "hidden %d not in {16,32,64}", a.hidden);
+  if (a.n_hidden != 3) return fail(NTBC_EFORMAT, "n_hidden %d != 3 (PAPER.md:331)", a.n_hidden);
+  if (a.F != 2) return fail(NTBC_EFORMAT, "features per level %d != 2 (PAPER.md:336)", a.F);
+  int want_e = 0, want_c = 0;
+  for (int i = 0; i < a.n_tex; i++) { want_e += a.fmt[i] == NTBC_BC1 ? 6 : 2; want_c += a.fmt[i] == NTBC_BC1 ? 3 : 1; }
+  if (n_e != want_e || n_c != want_c) return fail(NTBC_EFORMAT, "head widths %d/%d inconsistent with formats", n_e, n_c);
+  if (n_e > 48) return fail(NTBC_EFORMAT, "N_e = %d > 48 not supported", n_e);
+  for (int g = 0; g < 2; g++) {
+    if (a.levels[g] < 1 || a.levels[g] > kMaxLevels) return fail(NTBC_EFORMAT, "grid %d: %d levels not in [1,8]", g, a.levels[g]);
+    if (a.coarsest[g] < 2 || ((size_t)a.coarsest[g] << (a.levels[g] - 1)) > 8192)
+      return fail(NTBC_EFORMAT, "grid %d: bad resolution", g);
+  }
+  if (ep_in != 2 * a.levels[0] || col_in != 2 * a.levels[1]) return fail(NTBC_EFORMAT, "MLP input widths inconsistent");
+  size_t off = 96;
+  const size_t qp = off;
+  off += al16((size_t)(a.levels[0] + a.levels[1]) * 8);
+  int li = 0;
+  for (int g = 0; g < 2; g++)
+    for (int l = 0; l < a.levels[g]; l++, li++) {
+      if (qp + 8 * li + 8 > n) return fail(NTBC_EFORMAT, "blob truncated in quantization params");
+      memcpy(&a.s[g][l], b + qp + 8 * li, 4);
+      memcpy(&a.z[g][l], b + qp + 8 * li + 4, 4);
+    }
+  for (int g = 0; g < 2; g++)
+    for (int l = 0; l < a.levels[g]; l++) {
+      const size_t res = (size_t)a.coarsest[g] << l, sz = res * res * 2;
+      a.level_off[g][l] = off;
+      off += al16(sz);
+      if (off > n + 15) return fail(NTBC_EFORMAT, "blob truncated in grid %d level %d", g, l);
+    }
+  const int ins[2] = {ep_in, col_in}, outs[2] = {n_e, n_c};
+  for (int k = 0; k < 2; k++) {
+    a.dims[k][0] = ins[k];
+    a.dims[k][1] = a.dims[k][2] = a.dims[k][3] = a.hidden;
+    a.dims[k][4] = outs[k];
+    for (int l = 0; l < 4; l++) {
+      a.w_off[k][l] = off;
+      off += al16((size_t)a.dims[k][l] * a.dims[k][l + 1] * 2);
+      a.b_off[k][l] = off;
+      off += al16((size_t)a.dims[k][l + 1] * 2);
+    }
+  }
+  if (off > n + 15 || a.b_off[1][3] + (size_t)n_c * 2 > n) return fail(NTBC_EFORMAT, "blob truncated in MLP weights");
+  a.total = n;
+  return NTBC_OK;
+}
+
+bool same_arch(const Arch& x, const Arch& y) {
+  if (x.n_tex != y.n_tex || x.hidden != y.hidden || x.total != y.total) return false;
+  for (int i = 0; i < x.n_tex; i++) if (x.fmt[i] != y.fmt[i]) return false;
+  for (int g = 0; g < 2; g++) if (x.levels[g] != y.levels[g] || x.coarsest[g] != y.coarsest[g]) return false;
+  return true;
+}
+
+int round16(int v) { return (v + 15) & ~15; }
+
+}  // namespace
+
+struct ntbc_model_s {
+  int device;
+  Arch arch;
+  uint8_t* d_blob = nullptr;   // device copy of the whole blob (grid payloads read in place)
+  size_t blob_cap = 0;
+  uint8_t* d_img = nullptr;    // tcgen05 operand images of both nets
+  NetLayout net[2];
+  size_t img_bytes = 0;
+  // lazily sized scratch for ntbc_decode_material_host
+  uint8_t* d_scratch = nullptr;
+  size_t scratch_bytes = 0;
+};
+
+namespace {
+
+// B-operand image layout of both nets (K-major, bias folded as an extra K chunk)
+void layout_nets(ntbc_model_s* m) {
+  const Arch& a = m->arch;
+  uint32_t off = 0;
+  for (int k = 0; k < 2; k++) {
+    NetLayout& L = m->net[k];
+    L.img_off = off;
+    uint32_t o = 0;
+    for (int l = 0; l < 4; l++) {
+      const int kin16 = l == 0 ? 16 : a.hidden;
+      const int npad = l < 3 ? a.hidden : round16(a.dims[k][4]);
+      L.layer_off[l] = o;
+      o += (uint32_t)(npad * (kin16 + 16) * 2);
+    }
+    L.img_bytes = o;
+    L.n_out = a.dims[k][4];
+    L.n_out16 = round16(a.dims[k][4]);
+    off += o;
+  }
+  m->img_bytes = off;
+}
+
+ntbc_status upload(ntbc_model_s* m, const void* blob, size_t n, cudaStream_t st) {
+  const Arch& a = m->arch;
+  CUDA_TRY(cudaMemcpyAsync(m->d_blob, blob, n, cudaMemcpyHostToDevice, st));
+  for (int k = 0; k < 2; k++)
+    for (int l = 0; l < 4; l++) {
+      const int kin16 = l == 0 ? 16 : a.hidden, npad = l < 3 ? a.hidden : round16(a.dims[k][4]);
+      const int total = npad * (kin16 + 16);
+      relayout_kernel<<<(total + 255) / 256, 256, 0, st>>>(
+          reinterpret_cast<const __half*>(m->d_blob + a.w_off[k][l]), reinterpret_cast<const __half*>(m->d_blob + a.b_off[k][l]),
+          a.dims[k][l], a.dims[k][l + 1], kin16, npad, m->d_img + m->net[k].img_off + m->net[k].layer_off[l]);
+      g_launches++;
+    }
+  CUDA_TRY(cudaGetLastError());
+  return NTBC_OK;
+}
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) { cudaGetDevice(&prev); if (prev != d) cudaSetDevice(d); }
+  ~DevGuard() { int cur; cudaGetDevice(&cur); if (prev >= 0 && cur != prev) cudaSetDevice(prev); }
+};
+
+template <int H, int NWG, bool DUMP>
+ntbc_status launch_fused_t(const FusedParams& p, size_t smem, int grid, cudaStream_t st) {
+  auto kern = fused_decode_kernel<H, NWG, DUMP>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  kern<<<grid, NWG * 128, smem, st>>>(p);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return NTBC_OK;
+}
+
+size_t fused_smem(const FusedParams& p, int nwg) {
+  return (size_t)p.net[0].img_bytes + p.net[1].img_bytes + 4096 + (size_t)nwg * (p.a_bytes + p.pal_bytes) +
+         8 * (1 + nwg) + 16;
+}
+
+ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
+  const Arch& a = m->arch;
+  p.blob = m->d_blob;
+  p.img = m->d_img;
+  for (int g = 0; g < 2; g++) {
+    p.levels[g] = a.levels[g];
+    for (int l = 0; l < a.levels[g]; l++) {
+      p.lv[g][l].offset = (uint32_t)a.level_off[g][l];
+      p.lv[g][l].res = a.coarsest[g] << l;
+      p.lv[g][l].s = a.s[g][l];
+      p.lv[g][l].z = a.z[g][l];
+    }
+  }
+  p.net[0] = m->net[0];
+  p.net[1] = m->net[1];
+  p.n_tex = a.n_tex;
+  int eo = 0, co = 0;
+  for (int k = 0; k < a.n_tex; k++) {
+    p.fmt[k] = a.fmt[k];
+    p.ep_off[k] = eo;
+    p.col_off[k] = co;
+    eo += a.fmt[k] == NTBC_BC1 ? 6 : 2;
+    co += a.fmt[k] == NTBC_BC1 ? 3 : 1;
+  }
+  p.BW = p.W / 4;
+  p.BH = p.H / 4;
+  p.units_per_row = (p.BW + kUnitBlocks - 1) / kUnitBlocks;
+  p.n_units = p.units_per_row * (p.row_end - p.row_begin);
+  const int maxo = a.dims[0][4] > a.dims[1][4] ? a.dims[0][4] : a.dims[1][4];
+  const uint32_t a_kmajor = 128u * a.hidden * 2u, a_stage = 128u * 4u * (uint32_t)maxo;
+  p.a_bytes = (uint32_t)((std::max(a_kmajor, a_stage) + 127) & ~127u);
+  p.pal_bytes = (uint32_t)(a.n_tex * 128 * 32);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t cap = 227 * 1024;
+  const int nwg = fused_smem(p, 3) <= cap ? 3 : 2;
+  const size_t smem = fused_smem(p, nwg);
+  if (smem > cap) return fail(NTBC_EINVAL, "model needs %zu B of shared memory (> %zu)", smem, cap);
+  int grid = (p.n_units + nwg - 1) / nwg;
+  if (grid > sms) grid = sms;
+  if (grid < 1) grid = 1;
+#define NTBC_DISPATCH(HH)                                                                        \
+  if (a.hidden == HH) {                                                                          \
+    if (nwg == 3) return dump ? launch_fused_t<HH, 3, true>(p, smem, grid, st)                   \
+                              : launch_fused_t<HH, 3, false>(p, smem, grid, st);                 \
+    return dump ? launch_fused_t<HH, 2, true>(p, smem, grid, st) : launch_fused_t<HH, 2, false>(p, smem, grid, st); \
+  }
+  NTBC_DISPATCH(16)
+  NTBC_DISPATCH(32)
+  NTBC_DISPATCH(64)
+#undef NTBC_DISPATCH
+  return fail(NTBC_EINVAL, "unsupported hidden width");
+}
+
+ntbc_status check_dims(int W, int H, int r0, int r1) {
+  if (W <= 0 || H <= 0 || W % 4 || H % 4) return fail(NTBC_EINVAL, "width/height %dx%d must be positive multiples of 4", W, H);
+  if (r0 < 0 || r0 >= r1 || r1 > H / 4) return fail(NTBC_EINVAL, "block rows [%d,%d) not within [0,%d)", r0, r1, H / 4);
+  if ((long long)W * H > (1ll << 30)) return fail(NTBC_EINVAL, "texture too large");
+  return NTBC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ntbc_status ntbc_load_model(const void* blob, size_t nbytes, int cuda_device, ntbc_model* out) {
+  if (!out) return fail(NTBC_EINVAL, "out is NULL");
+  *out = nullptr;
+  Arch a;
+  ntbc_status st = parse(blob, nbytes, a);
+  if (st) return st;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (cuda_device < 0 || cuda_device >= ndev) return fail(NTBC_EINVAL, "cuda_device %d out of range", cuda_device);
+  DevGuard dg(cuda_device);
+  auto* m = new ntbc_model_s();
+  m->device = cuda_device;
+  m->arch = a;
+  layout_nets(m);
+  if (cudaMalloc(&m->d_blob, al16(nbytes)) != cudaSuccess || cudaMalloc(&m->d_img, m->img_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    ntbc_free_model(m);
+    return fail(NTBC_ENOMEM, "device allocation of %zu bytes failed", nbytes + m->img_bytes);
+  }
+  m->blob_cap = al16(nbytes);
+  cudaMemset(m->d_img, 0, m->img_bytes);
+  st = upload(m, blob, nbytes, 0);
+  if (st == NTBC_OK && cudaDeviceSynchronize() != cudaSuccess) st = fail(NTBC_ECUDA, "model upload: %s", cudaGetErrorString(cudaGetLastError()));
+  if (st) { ntbc_free_model(m); return st; }
+  *out = m;
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_model_upload_async(ntbc_model m, const void* blob, size_t nbytes, void* stream) {
+  if (!m || !blob) return fail(NTBC_EINVAL, "NULL argument");
+  Arch a;
+  ntbc_status st = parse(blob, nbytes, a);
+  if (st) return st;
+  if (!same_arch(a, m->arch)) return fail(NTBC_EMISMATCH, "blob architecture differs from the loaded model");
+  DevGuard dg(m->device);
+  m->arch = a;  // same layout; refresh the per-level (s, z)
+  return upload(m, blob, nbytes, (cudaStream_t)stream);
+}
+
+ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out) {
+  if (!m || !out) return fail(NTBC_EINVAL, "NULL argument");
+  const Arch& a = m->arch;
+  memset(out, 0, sizeof *out);
+  out->n_textures = a.n_tex;
+  for (int i = 0; i < a.n_tex; i++) out->fmt[i] = a.fmt[i];
+  out->hidden = a.hidden;
+  out->n_hidden = a.n_hidden;
+  out->n_endpoint_out = a.dims[0][4];
+  out->n_color_out = a.dims[1][4];
+  out->block_levels = a.levels[0];
+  out->block_coarsest = a.coarsest[0];
+  out->texel_levels = a.levels[1];
+  out->texel_coarsest = a.coarsest[1];
+  out->features = a.F;
+  out->device_bytes = m->blob_cap + m->img_bytes + m->scratch_bytes;
+  return NTBC_OK;
+}
+
+void ntbc_free_model(ntbc_model m) {
+  if (!m) return;
+  DevGuard dg(m->device);
+  cudaFree(m->d_blob);
+  cudaFree(m->d_img);
+  cudaFree(m->d_scratch);
+  delete m;
+}
+
+ntbc_status ntbc_decode_material(const ntbc_model* models, int n_models, int width, int height, int r0, int r1,
+                                 void* const* out_blocks, void* stream) {
+  if (!models || !out_blocks) return fail(NTBC_EINVAL, "NULL argument");
+  if (n_models < 1 || n_models > 2) return fail(NTBC_EINVAL, "n_models %d not in {1,2}", n_models);
+  ntbc_status st = check_dims(width, height, r0, r1);
+  if (st) return st;
+  for (int i = 0; i < n_models; i++) if (!models[i]) return fail(NTBC_EINVAL, "model %d is NULL", i);
+  if (n_models == 2) {  // conservative pair: one all-BC1 model and one all-BC4 model
+    auto all = [](const Arch& a, int f) { for (int k = 0; k < a.n_tex; k++) if (a.fmt[k] != f) return false; return true; };
+    const Arch &x = models[0]->arch, &y = models[1]->arch;
+    if (!((all(x, NTBC_BC1) && all(y, NTBC_BC4)) || (all(x, NTBC_BC4) && all(y, NTBC_BC1))))
+      return fail(NTBC_EMISMATCH, "conservative pair must be one all-BC1 and one all-BC4 model");
+    if (models[0]->device != models[1]->device) return fail(NTBC_EMISMATCH, "models on different devices");
+  }
+  int t = 0;
+  for (int i = 0; i < n_models; i++) {
+    const ntbc_model_s* m = models[i];
+    DevGuard dg(m->device);
+    FusedParams p{};
+    p.W = width; p.H = height; p.row_begin = r0; p.row_end = r1;
+    for (int k = 0; k < m->arch.n_tex; k++, t++) {
+      if (!out_blocks[t] || ((uintptr_t)out_blocks[t] & 15)) return fail(NTBC_EINVAL, "out_blocks[%d] NULL or not 16-B aligned", t);
+      p.out[k] = (uint64_t*)out_blocks[t];
+    }
+    st = launch_fused(m, p, false, (cudaStream_t)stream);
+    if (st) return st;
+  }
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, const void* const* blobs,
+                                      const size_t* blob_sizes, int width, int height, void* const* host_out,
+                                      void* stream) {
+  if (!models || !blobs || !blob_sizes || !host_out) return fail(NTBC_EINVAL, "NULL argument");
+  if (n_models < 1 || n_models > 2) return fail(NTBC_EINVAL, "n_models %d not in {1,2}", n_models);
+  ntbc_status st = check_dims(width, height, 0, height / 4);
+  if (st) return st;
+  const size_t plane = (size_t)(width / 4) * (height / 4) * 8;
+  void* dev_out[2 * kMaxTex];
+  int t = 0;
+  for (int i = 0; i < n_models; i++) {
+    ntbc_model_s* m = models[i];
+    if (!m) return fail(NTBC_EINVAL, "model %d is NULL", i);
+    DevGuard dg(m->device);
+    const size_t need = plane * m->arch.n_tex;
+    if (m->scratch_bytes < need) {
+      cudaFree(m->d_scratch);
+      m->d_scratch = nullptr;
+      m->scratch_bytes = 0;
+      if (cudaMalloc(&m->d_scratch, need) != cudaSuccess) { cudaGetLastError(); return fail(NTBC_ENOMEM, "scratch %zu B", need); }
+      m->scratch_bytes = need;
+    }
+    st = ntbc_model_upload_async(m, blobs[i], blob_sizes[i], stream);
+    if (st) return st;
+    for (int k = 0; k < m->arch.n_tex; k++) dev_out[t++] = m->d_scratch + k * plane;
+  }
+  st = ntbc_decode_material(models, n_models, width, height, 0, height / 4, dev_out, stream);
+  if (st) return st;
+  for (int k = 0; k < t; k++) {
+    if (!host_out[k]) return fail(NTBC_EINVAL, "host_out[%d] is NULL", k);
+    CUDA_TRY(cudaMemcpyAsync(host_out[k], dev_out[k], plane, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  }
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_decode_bc(const void* blocks, ntbc_format fmt, int width, int height, float* out, void* stream) {
+  if (!blocks || !out) return fail(NTBC_EINVAL, "NULL argument");
+  if (fmt != NTBC_BC1 && fmt != NTBC_BC4) return fail(NTBC_EINVAL, "bad format %d", (int)fmt);
+  ntbc_status st = check_dims(width, height, 0, height / 4);
+  if (st) return st;
+  const long long n = (long long)width * height;
+  const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+  decode_bc_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint64_t*)blocks, (int)fmt, width, height, out);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_debug_mlp(ntbc_model m, int width, int height, int r0, int r1, float* endpoints, float* colors,
+                           void* stream) {
+  if (!m || !endpoints || !colors) return fail(NTBC_EINVAL, "NULL argument");
+  ntbc_status st = check_dims(width, height, r0, r1);
+  if (st) return st;
+  DevGuard dg(m->device);
+  FusedParams p{};
+  p.W = width; p.H = height; p.row_begin = r0; p.row_end = r1;
+  p.dump_ep = endpoints;
+  p.dump_col = colors;
+  return launch_fused(m, p, true, (cudaStream_t)stream);
+}
+
+ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const float* colors, int width, int height,
+                      int r0, int r1, void* const* out_blocks, void* stream) {
+  if (!fmts || !endpoints || !colors || !out_blocks) return fail(NTBC_EINVAL, "NULL argument");
+  if (n_tex < 1 || n_tex > kMaxTex) return fail(NTBC_EINVAL, "n_textures %d not in [1,8]", n_tex);
+  ntbc_status st = check_dims(width, height, r0, r1);
+  if (st) return st;
+  PackParams p{};
+  p.ep = endpoints; p.col = colors; p.W = width; p.BW = width / 4; p.rows = r1 - r0; p.n_tex = n_tex;
+  int eo = 0, co = 0;
+  for (int k = 0; k < n_tex; k++) {
+    if (fmts[k] != NTBC_BC1 && fmts[k] != NTBC_BC4) return fail(NTBC_EINVAL, "bad format %d", fmts[k]);
+    if (!out_blocks[k] || ((uintptr_t)out_blocks[k] & 7)) return fail(NTBC_EINVAL, "out_blocks[%d] NULL or misaligned", k);
+    p.fmt[k] = fmts[k]; p.ep_off[k] = eo; p.col_off[k] = co; p.out[k] = (uint64_t*)out_blocks[k];
+    eo += fmts[k] == NTBC_BC1 ? 6 : 2;
+    co += fmts[k] == NTBC_BC1 ? 3 : 1;
+  }
+  p.n_e = eo; p.n_c = co;
+  const long long pairs = (long long)((p.BW + 1) / 2) * p.rows;
+  const int grid = (int)std::min<long long>((pairs + 7) / 8, 148 * 8);
+  pack_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(p);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_debug_mma(const void* A, const void* B, const float* C, float* D, int K, int N, void* stream) {
+  if (!A || !B || !D) return fail(NTBC_EINVAL, "NULL argument");
+  if (K <= 0 || K % 16 || K > 128 || (N != 16 && N != 32 && N != 64)) return fail(NTBC_EINVAL, "bad K=%d N=%d", K, N);
+  const size_t smem = 128 * K * 2 + 64 * K * 2 + 64;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_TRY(cudaFuncSetAttribute(mma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  mma_probe_kernel<<<1, 128, smem, (cudaStream_t)stream>>>((const __half*)A, (const __half*)B, C, D, K, N);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return NTBC_OK;
+}
+
+uint64_t ntbc_launch_count(void) { return g_launches.load(); }
+
+const char* ntbc_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

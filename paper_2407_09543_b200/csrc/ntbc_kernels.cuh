@@ -1,0 +1,472 @@
+// ntbc_kernels.cuh -- the three sm_100a kernels of the NTBC inference hot path:
+//   (1) fused_decode_kernel: grid dequant + multi-resolution bilinear sampling (rows a1-a2),
+//       endpoint and colour MLPs on tcgen05 tensor cores with TMEM accumulators (a3-a4),
+//       endpoint quantization, palettes, per-texel argmax, warp-ballot bit packing (a5-a8);
+//   (2) pack_kernel: rows a5-a8 standalone, fed fp32 MLP outputs (HBM-bound);
+//   (3) decode_bc_kernel: BC1/BC4 -> fp32 texels (row a9, verification).
+// Plus relayout_kernel (model upload) and mma_probe_kernel (pins the tensor-core summation, R10).
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+
+#include "bc_device.cuh"
+#include "sm100.cuh"
+
+namespace ntbc {
+
+constexpr int kMaxTex = 8;
+constexpr int kMaxLevels = 8;
+constexpr int kUnitBlocks = 128;  // block positions per work unit = rows of one endpoint MMA tile
+constexpr int kFmtBC1 = 1;
+
+struct GridLevel {
+  uint32_t offset;  // byte offset of the level payload [res][res][2] in the model blob (device copy)
+  int res;
+  float s;          // Eq.2 scale
+  int z;            // Eq.2 zero point
+};
+
+struct NetLayout {
+  uint32_t img_off;       // byte offset of this net's operand image inside Model::d_img
+  uint32_t img_bytes;
+  uint32_t layer_off[4];  // byte offset of layer l's B operand [N_l][K_l] inside the net image
+  int n_out, n_out16;
+};
+
+struct FusedParams {
+  const uint8_t* blob;    // device copy of the .ntbc blob (grid payloads are read from here)
+  const uint8_t* img;     // device operand images (both nets, tcgen05 K-major layout, bias folded)
+  GridLevel lv[2][kMaxLevels];
+  int levels[2];
+  NetLayout net[2];
+  int W, H, BW, BH, row_begin, row_end, units_per_row, n_units;
+  int n_tex;
+  int fmt[kMaxTex], ep_off[kMaxTex], col_off[kMaxTex];
+  uint64_t* out[kMaxTex];
+  float* dump_ep;   // DUMP mode: [rows][BW][N_e]
+  float* dump_col;  // DUMP mode: [rows*4][W][N_c]
+  uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
+};
+
+// ---------------------------------------------------------------- a1-a2: coordinates + grid encode
+// Vertex-centred bilinear lookup of one level (R1), Eq.2 dequantization (R6), lerp = fma(t, b-a, a)
+__device__ __forceinline__ void level_lookup(const uint8_t* blob, const GridLevel& L, float pu, float pv,
+                                             float& f0, float& f1) {
+  const float rm1 = (float)(L.res - 1);
+  const float X = __fmul_rn(pu, rm1), Y = __fmul_rn(pv, rm1);
+  int i0 = (int)floorf(X), j0 = (int)floorf(Y);
+  i0 = max(0, min(i0, L.res - 2));
+  j0 = max(0, min(j0, L.res - 2));
+  const float fx = __fsub_rn(X, (float)i0), fy = __fsub_rn(Y, (float)j0);
+  const uint16_t* g = reinterpret_cast<const uint16_t*>(blob + L.offset);
+  const uint32_t q00 = __ldg(g + j0 * L.res + i0), q10 = __ldg(g + j0 * L.res + i0 + 1);
+  const uint32_t q01 = __ldg(g + (j0 + 1) * L.res + i0), q11 = __ldg(g + (j0 + 1) * L.res + i0 + 1);
+#define NTBC_DQ(q, sh) __fmul_rn(L.s, (float)((int)(((q) >> (sh)) & 0xFFu) - L.z))
+#define NTBC_LERP(a, b, t) __fmaf_rn((t), __fsub_rn((b), (a)), (a))
+  {
+    const float v00 = NTBC_DQ(q00, 0), v10 = NTBC_DQ(q10, 0), v01 = NTBC_DQ(q01, 0), v11 = NTBC_DQ(q11, 0);
+    f0 = NTBC_LERP(NTBC_LERP(v00, v10, fx), NTBC_LERP(v01, v11, fx), fy);
+  }
+  {
+    const float v00 = NTBC_DQ(q00, 8), v10 = NTBC_DQ(q10, 8), v01 = NTBC_DQ(q01, 8), v11 = NTBC_DQ(q11, 8);
+    f1 = NTBC_LERP(NTBC_LERP(v00, v10, fx), NTBC_LERP(v01, v11, fx), fy);
+  }
+#undef NTBC_DQ
+#undef NTBC_LERP
+}
+
+// 16 features (levels coarse->fine, 2 per level, R3) of grid g at (pu, pv), rounded to fp16 and
+// written as row `row` of a K-major [128][K] operand (columns 0..15; unused levels are zero).
+__device__ __forceinline__ void write_feature_row(const FusedParams& p, int g, float pu, float pv, uint8_t* A,
+                                                  int row, int K) {
+  uint32_t h[8];
+#pragma unroll
+  for (int l = 0; l < kMaxLevels; l++) {
+    float f0 = 0.0f, f1 = 0.0f;
+    if (l < p.levels[g]) level_lookup(p.blob, p.lv[g][l], pu, pv, f0, f1);
+    const __half2 v = __floats2half2_rn(f0, f1);
+    h[l] = *reinterpret_cast<const uint32_t*>(&v);
+  }
+  *reinterpret_cast<uint4*>(A + kmajor_offset(row, 0, K)) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(A + kmajor_offset(row, 8, K)) = make_uint4(h[4], h[5], h[6], h[7]);
+}
+
+// ---------------------------------------------------------------- TMEM load helper (x16 columns)
+__device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// Issue one layer of the MLP for the 128 rows of a work group (called by ONE thread):
+// bias chunk first (A = ones tile, B = bias column; overwrites D), then the K/16 activation chunks
+// in increasing k (accumulate) -- the summation order pinned by R10.
+__device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, int K_A, uint32_t ones_base,
+                                            uint32_t b_base, int kin16, int N) {
+  const int K_B = kin16 + 16;
+  const uint32_t idesc = idesc_f16_f32(128, N);
+  mma_f16(tmem_d, smem_desc(ones_base, 128, 256), smem_desc(b_base + (kin16 / 16) * 256, 128, K_B * 16), idesc, 0u);
+  for (int c = 0; c < kin16 / 16; c++)
+    mma_f16(tmem_d, smem_desc(a_base + c * 256, 128, K_A * 16), smem_desc(b_base + c * 256, 128, K_B * 16), idesc,
+            1u);
+}
+
+// ---------------------------------------------------------------- kernel (1): fused decode
+// One CTA per SM, NWG independent 128-thread work groups; each work group owns 64 TMEM columns,
+// an A-operand buffer and a palette buffer, and loops over work units of 128 block positions of
+// one block row: one endpoint tile (128 blocks) then up to 16 colour tiles (8 blocks = 128 texels).
+template <int H, int NWG, bool DUMP>
+__global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5, lane = tid & 31;
+
+  // ---- carve shared memory
+  uint8_t* img_e = smem;                                          // endpoint net operand image
+  uint8_t* img_c = smem + p.net[0].img_bytes;                     // colour net operand image
+  uint8_t* ones = img_c + p.net[1].img_bytes;                     // [128][16] K-major, column 0 = 1.0
+  uint8_t* wg_base = ones + 4096 + wg * (p.a_bytes + p.pal_bytes);
+  uint8_t* A = wg_base;                                           // [128][H] K-major fp16 / fp32 staging
+  float* stage = reinterpret_cast<float*>(A);                     // [ch][128] fp32 (after the last MMA)
+  float* pal = reinterpret_cast<float*>(wg_base + p.a_bytes);     // [tex][128 blocks][8] fp32
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ones + 4096 + NWG * (p.a_bytes + p.pal_bytes));
+  uint64_t* bar_w = bars;                                         // weights landed
+  uint64_t* bar_mma = bars + 1 + wg;                              // this work group's MMA completion
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + NWG);
+
+  if (tid == 0) {
+    mbar_init(bar_w, 1);
+    for (int g = 0; g < NWG; g++) mbar_init(bars + 1 + g, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, NWG <= 2 ? 128 : 256);
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // ---- stage both nets' operand images with the bulk-copy (TMA) engine
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar_w, p.net[0].img_bytes + p.net[1].img_bytes);
+    bulk_g2s(img_e, p.img + p.net[0].img_off, p.net[0].img_bytes, bar_w);
+    bulk_g2s(img_c, p.img + p.net[1].img_off, p.net[1].img_bytes, bar_w);
+  }
+  if (tid < 128) {  // the constant ones tile used to fold the bias into the MMA
+    const uint4 c0 = make_uint4(0x3C00u, 0u, 0u, 0u), z = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(ones + kmajor_offset(tid, 0, 16)) = c0;
+    *reinterpret_cast<uint4*>(ones + kmajor_offset(tid, 8, 16)) = z;
+  }
+  fence_async_smem();
+  mbar_wait(bar_w, 0);
+  __syncthreads();
+
+  const uint32_t tm = tmem_base + (uint32_t)(wg * 64);                    // D columns of this group
+  const uint32_t tm_row = tm + ((uint32_t)(32 * (warp & 3)) << 16);       // this warp's TMEM lanes
+  const uint32_t a_base = smem_u32(A), ones_base = smem_u32(ones);
+  const uint32_t img_base[2] = {smem_u32(img_e), smem_u32(img_c)};
+  const int bar_id = 1 + wg;
+  uint32_t phase = 0;
+
+  // run the 4-layer MLP of net `n` on the A rows already written; leaves the output layer in TMEM
+  auto run_mlp = [&](int n) {
+#pragma unroll 1
+    for (int l = 0; l < 4; l++) {
+      fence_async_smem();
+      tc_fence_before();
+      named_bar_sync(bar_id, 128);
+      if (r == 0) {
+        tc_fence_after();
+        const int kin16 = l == 0 ? 16 : H;
+        const int N = l < 3 ? H : p.net[n].n_out16;
+        issue_layer(tm, a_base, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
+        mma_commit(bar_mma);
+      }
+      mbar_wait(bar_mma, phase);
+      phase ^= 1u;
+      tc_fence_after();
+      if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10)
+        uint32_t acc[H];
+#pragma unroll
+        for (int c = 0; c < H / 16; c++) tmem_ld16p(tm_row + c * 16, acc + c * 16);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k8 = 0; k8 < H / 8; k8++) {
+          uint32_t hv[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const float a = selu(__uint_as_float(acc[k8 * 8 + 2 * j]));
+            const float b = selu(__uint_as_float(acc[k8 * 8 + 2 * j + 1]));
+            const __half2 v = __floats2half2_rn(a, b);
+            hv[j] = *reinterpret_cast<const uint32_t*>(&v);
+          }
+          *reinterpret_cast<uint4*>(A + kmajor_offset(r, k8 * 8, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+        }
+      }
+    }
+  };
+  // output layer epilogue: sigmoid of the n_out columns -> fp32 staging [ch][128] (own row only)
+  auto stage_outputs = [&](int n) {
+    uint32_t acc[48];  // n_out16 <= 48 is enforced at load
+    const int n16 = p.net[n].n_out16;
+#pragma unroll
+    for (int c = 0; c < 3; c++)
+      if (c * 16 < n16) tmem_ld16p(tm_row + c * 16, acc + c * 16);
+    tmem_wait_ld();
+    // the output MMA has completed (mbarrier), so A may be overwritten by the fp32 staging
+    const int no = p.net[n].n_out;
+#pragma unroll
+    for (int ch = 0; ch < 48; ch++)
+      if (ch < no) stage[ch * 128 + r] = sigmoid(__uint_as_float(acc[ch]));
+  };
+
+#pragma unroll 1
+  for (int u = blockIdx.x * NWG + wg; u < p.n_units; u += gridDim.x * NWG) {
+    const int by = p.row_begin + u / p.units_per_row;
+    const int bx0 = (u % p.units_per_row) * kUnitBlocks;
+    const int nvalid = min(kUnitBlocks, p.BW - bx0);
+    const size_t out_row = (size_t)(by - p.row_begin) * p.BW;
+
+    // ================= endpoint tile: row r = block (bx0 + r, by)  (rows a1-a3, a5-a6)
+    named_bar_sync(bar_id, 128);  // previous tile's readers of A / staging / palettes are done
+    {
+      const float s = __fdiv_rn(__fadd_rn((float)(bx0 + r), 0.5f), (float)p.BW);
+      const float t = __fdiv_rn(__fadd_rn((float)by, 0.5f), (float)p.BH);
+      write_feature_row(p, 0, s, t, A, r, H);
+    }
+    run_mlp(0);
+    stage_outputs(0);
+    if (DUMP) {
+      if (r < nvalid)
+        for (int ch = 0; ch < p.net[0].n_out; ch++)
+          p.dump_ep[(out_row + bx0 + r) * p.net[0].n_out + ch] = stage[ch * 128 + r];
+    } else {
+      for (int k = 0; k < p.n_tex; k++) {
+        const int eo = p.ep_off[k];
+        float4* slot = reinterpret_cast<float4*>(pal + ((size_t)k * 128 + r) * 8);
+        if (p.fmt[k] == kFmtBC1) {
+          float ep[6], e0[3], e1[3];
+#pragma unroll
+          for (int c = 0; c < 6; c++) ep[c] = stage[(eo + c) * 128 + r];
+          const uint32_t hdr = quant_bc1(ep, e0, e1);
+          slot[0] = make_float4(e0[0], e0[1], e0[2], e1[0]);
+          slot[1] = make_float4(e1[1], e1[2], __uint_as_float(hdr), 0.0f);
+        } else {
+          float ep[2], e0, e1;
+          ep[0] = stage[eo * 128 + r];
+          ep[1] = stage[(eo + 1) * 128 + r];
+          const uint32_t hdr = quant_bc4(ep, e0, e1);
+          slot[0] = make_float4(e0, e1, __uint_as_float(hdr), 0.0f);
+        }
+      }
+    }
+
+    // ================= colour tiles: row r = texel (r & 15) of block 8j + (r >> 4)  (a1-a2, a4, a6-a8)
+#pragma unroll 1
+    for (int j = 0; j < kUnitBlocks / 8 && 8 * j < nvalid; j++) {
+      const int b = 8 * j + (r >> 4), i = r & 15;
+      const int bx = bx0 + b, x = 4 * bx + (i & 3), y = 4 * by + (i >> 2);
+      named_bar_sync(bar_id, 128);
+      {
+        const float pu = __fdiv_rn(__fadd_rn((float)x, 0.5f), (float)p.W);
+        const float pv = __fdiv_rn(__fadd_rn((float)y, 0.5f), (float)p.H);
+        write_feature_row(p, 1, pu, pv, A, r, H);
+      }
+      run_mlp(1);
+      stage_outputs(1);
+      if (DUMP) {
+        if (b < nvalid)
+          for (int ch = 0; ch < p.net[1].n_out; ch++)
+            p.dump_col[(((size_t)(y - 4 * p.row_begin)) * p.W + x) * p.net[1].n_out + ch] = stage[ch * 128 + r];
+      } else {
+        for (int k = 0; k < p.n_tex; k++) {
+          const int co = p.col_off[k];
+          const float4* slot = reinterpret_cast<const float4*>(pal + ((size_t)k * 128 + b) * 8);
+          uint64_t word;
+          if (p.fmt[k] == kFmtBC1) {
+            const float4 s0 = slot[0], s1 = slot[1];
+            const float e0[3] = {s0.x, s0.y, s0.z}, e1[3] = {s0.w, s1.x, s1.y};
+            const uint32_t hdr = __float_as_uint(s1.z);
+            const float c[3] = {stage[co * 128 + r], stage[(co + 1) * 128 + r], stage[(co + 2) * 128 + r]};
+            const uint32_t code = bc1_code(c, e0, e1, (hdr & 0xFFFFu) == (hdr >> 16));
+            word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
+          } else {
+            const float4 s0 = slot[0];
+            const uint32_t hdr = __float_as_uint(s0.z);
+            const uint32_t code = bc4_code(stage[co * 128 + r], s0.x, s0.y, (hdr & 0xFFu) > (hdr >> 8));
+            word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
+          }
+          if ((lane & 15) == 0 && b < nvalid) p.out[k][out_row + bx] = word;
+        }
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem_base, NWG <= 2 ? 128 : 256);
+}
+
+// ---------------------------------------------------------------- kernel (2): standalone pack (a5-a8)
+struct PackParams {
+  const float* ep;   // [rows][BW][N_e]
+  const float* col;  // [rows*4][W][N_c]
+  int W, BW, rows, n_e, n_c, n_tex;
+  int fmt[kMaxTex], ep_off[kMaxTex], col_off[kMaxTex];
+  uint64_t* out[kMaxTex];
+};
+// one warp = two horizontally adjacent blocks; lane = texel (lane & 15) of block (lane >> 4)
+__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams p) {
+  const int lane = threadIdx.x & 31;
+  const int pairs_per_row = (p.BW + 1) / 2;
+  const long long n_pairs = (long long)pairs_per_row * p.rows;
+  for (long long w = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < n_pairs;
+       w += (long long)gridDim.x * (blockDim.x / 32)) {
+    const int row = (int)(w / pairs_per_row);
+    const int bx = (int)(w % pairs_per_row) * 2 + (lane >> 4);
+    const bool valid = bx < p.BW;
+    const int bxc = valid ? bx : p.BW - 1;
+    const int i = lane & 15, x = 4 * bxc + (i & 3), y = 4 * row + (i >> 2);
+    const float* e = p.ep + ((size_t)row * p.BW + bxc) * p.n_e;
+    const float* c = p.col + ((size_t)y * p.W + x) * p.n_c;
+    for (int k = 0; k < p.n_tex; k++) {
+      uint64_t word;
+      if (p.fmt[k] == kFmtBC1) {
+        float ep[6], e0[3], e1[3];
+#pragma unroll
+        for (int q = 0; q < 6; q++) ep[q] = __ldg(e + p.ep_off[k] + q);
+        const uint32_t hdr = quant_bc1(ep, e0, e1);
+        const float cc[3] = {__ldg(c + p.col_off[k]), __ldg(c + p.col_off[k] + 1), __ldg(c + p.col_off[k] + 2)};
+        const uint32_t code = bc1_code(cc, e0, e1, (hdr & 0xFFFFu) == (hdr >> 16));
+        word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
+      } else {
+        float ep[2], e0, e1;
+        ep[0] = __ldg(e + p.ep_off[k]);
+        ep[1] = __ldg(e + p.ep_off[k] + 1);
+        const uint32_t hdr = quant_bc4(ep, e0, e1);
+        const uint32_t code = bc4_code(__ldg(c + p.col_off[k]), e0, e1, (hdr & 0xFFu) > (hdr >> 8));
+        word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
+      }
+      if ((lane & 15) == 0 && valid) p.out[k][(size_t)row * p.BW + bx] = word;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kernel (3): BC decode (a9)
+__global__ void __launch_bounds__(256) decode_bc_kernel(const uint64_t* __restrict__ blocks, int fmt, int W, int H,
+                                                         float* __restrict__ out) {
+  const long long n = (long long)W * H;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(t % W), y = (int)(t / W);
+    const int BW = W / 4;
+    const uint64_t blk = __ldg(blocks + (size_t)(y >> 2) * BW + (x >> 2));
+    const int i = (y & 3) * 4 + (x & 3);
+    if (fmt == kFmtBC1) {
+      const uint32_t c0 = (uint32_t)(blk & 0xFFFF), c1 = (uint32_t)((blk >> 16) & 0xFFFF);
+      const uint32_t code = (uint32_t)(blk >> (32 + 2 * i)) & 3u;
+      float e0[3], e1[3];
+      e0[0] = __fdiv_rn((float)(c0 >> 11), 31.0f); e0[1] = __fdiv_rn((float)((c0 >> 5) & 63), 63.0f);
+      e0[2] = __fdiv_rn((float)(c0 & 31), 31.0f);
+      e1[0] = __fdiv_rn((float)(c1 >> 11), 31.0f); e1[1] = __fdiv_rn((float)((c1 >> 5) & 63), 63.0f);
+      e1[2] = __fdiv_rn((float)(c1 & 31), 31.0f);
+      float v[3];
+#pragma unroll
+      for (int ch = 0; ch < 3; ch++) {
+        if (c0 > c1) {  // 4-colour mode: code -> linear n = [0,3,1,2]
+          const int n_lin = (0x2130 >> (4 * code)) & 3;
+          const float w = __fdiv_rn((float)n_lin, 3.0f);
+          v[ch] = interp(w, e0[ch], e1[ch]);
+        } else {        // DirectX 3-colour mode (never emitted by the encoder, R12)
+          v[ch] = code == 0 ? e0[ch] : code == 1 ? e1[ch] : code == 2 ? __fmaf_rn(0.5f, e1[ch], __fmul_rn(0.5f, e0[ch])) : 0.0f;
+        }
+      }
+      float* o = out + (size_t)t * 3;
+      o[0] = v[0]; o[1] = v[1]; o[2] = v[2];
+    } else {
+      const uint32_t E0 = (uint32_t)(blk & 0xFF), E1 = (uint32_t)((blk >> 8) & 0xFF);
+      const uint32_t code = (uint32_t)(blk >> (16 + 3 * i)) & 7u;
+      const float e0 = __fdiv_rn((float)E0, 255.0f), e1 = __fdiv_rn((float)E1, 255.0f);
+      float v;
+      if (E0 > E1) {  // code -> linear n: 0->0, 1->7, c->c-1
+        const int n_lin = code == 0 ? 0 : code == 1 ? 7 : (int)code - 1;
+        v = interp(__fdiv_rn((float)n_lin, 7.0f), e0, e1);
+      } else {        // code -> linear n: 0->1, 1->6, 2..5->same, 6->0 (0.0), 7->7 (1.0)
+        if (code == 6) v = 0.0f;
+        else if (code == 7) v = 1.0f;
+        else {
+          const int n_lin = code == 0 ? 1 : code == 1 ? 6 : (int)code;
+          v = interp(__fdiv_rn((float)(n_lin - 1), 5.0f), e0, e1);
+        }
+      }
+      out[t] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- model upload: operand relayout
+// B operand of one layer: [Npad][K_B] K-major (sm100.cuh kmajor_offset), K_B = kin16 + 16,
+// W[k][n] for k < kin, n < nout; bias in column kin16; zeros elsewhere.
+__global__ void relayout_kernel(const __half* __restrict__ W, const __half* __restrict__ b, int kin, int nout,
+                                int kin16, int npad, uint8_t* __restrict__ dst) {
+  const int K_B = kin16 + 16;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= npad * K_B) return;
+  const int n = t / K_B, k = t % K_B;
+  __half v = __float2half_rn(0.0f);
+  if (n < nout && k < kin) v = W[(size_t)k * nout + n];
+  else if (n < nout && k == kin16) v = b[n];
+  *reinterpret_cast<__half*>(dst + kmajor_offset(n, k, K_B)) = v;
+}
+
+// ---------------------------------------------------------------- tensor-core summation probe (R10)
+__global__ void __launch_bounds__(128, 1) mma_probe_kernel(const __half* __restrict__ A, const __half* __restrict__ B,
+                                                           const float* __restrict__ C, float* __restrict__ D, int K,
+                                                           int N) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + 128 * K * 2;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 64 * K * 2);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int r = threadIdx.x, warp = r >> 5;
+  for (int k = 0; k < K; k++) {
+    *reinterpret_cast<__half*>(sA + kmajor_offset(r, k, K)) = A[(size_t)r * K + k];
+    if (r < N) *reinterpret_cast<__half*>(sB + kmajor_offset(r, k, K)) = B[(size_t)r * K + k];
+  }
+  fence_async_smem();
+  if (r == 0) { mbar_init(bar, 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc(slot, 64);
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *slot, trow = tbase + ((uint32_t)(32 * warp) << 16);
+  if (C) {
+    for (int c = 0; c < N; c += 16) {
+      uint32_t v[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) v[j] = __float_as_uint(C[(size_t)r * N + c + j]);
+      tmem_st16(trow + c, v);
+    }
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (r == 0) {
+    tc_fence_after();
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB), idesc = idesc_f16_f32(128, N);
+    for (int c = 0; c < K / 16; c++)
+      mma_f16(tbase, smem_desc(a0 + c * 256, 128, K * 16), smem_desc(b0 + c * 256, 128, K * 16), idesc,
+              (C != nullptr || c > 0) ? 1u : 0u);
+    mma_commit(bar);
+  }
+  mbar_wait(bar, 0);
+  tc_fence_after();
+  for (int c = 0; c < N; c += 16) {
+    uint32_t v[16];
+    tmem_ld16p(trow + c, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; j++) D[(size_t)r * N + c + j] = __uint_as_float(v[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 64);
+}
+
+}  // namespace ntbc

@@ -1,0 +1,182 @@
+"""Thin ctypes binding of libntbc.so (include/ntbc.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libntbc.so.  There is no
+CPU fallback: if the library is missing this module raises at import time.
+PyTorch supplies device memory (tensors) and streams; pointers are passed as
+integers.  Names follow the C ABI (ntbc_<name> -> <name>).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libntbc.so")
+BC1, BC4 = 1, 4
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(there is no CPU fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+_vp, _i, _sz = C.c_void_p, C.c_int, C.c_size_t
+
+
+class _Info(C.Structure):
+    _fields_ = [("n_textures", C.c_int), ("fmt", C.c_int * 8), ("hidden", C.c_int), ("n_hidden", C.c_int),
+                ("n_endpoint_out", C.c_int), ("n_color_out", C.c_int), ("block_levels", C.c_int),
+                ("block_coarsest", C.c_int), ("texel_levels", C.c_int), ("texel_coarsest", C.c_int),
+                ("features", C.c_int), ("device_bytes", C.c_size_t)]
+
+
+_SIGS = {
+    "ntbc_load_model": (_i, [_vp, _sz, _i, C.POINTER(_vp)]),
+    "ntbc_model_upload_async": (_i, [_vp, _vp, _sz, _vp]),
+    "ntbc_model_get_info": (_i, [_vp, C.POINTER(_Info)]),
+    "ntbc_free_model": (None, [_vp]),
+    "ntbc_decode_material": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
+    "ntbc_decode_material_host": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _vp]),
+    "ntbc_decode_bc": (_i, [_vp, _i, _i, _i, _vp, _vp]),
+    "ntbc_debug_mlp": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
+    "ntbc_pack": (_i, [_i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
+    "ntbc_debug_mma": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp]),
+    "ntbc_launch_count": (C.c_uint64, []),
+    "ntbc_last_error": (C.c_char_p, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+class NtbcError(RuntimeError):
+    pass
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise NtbcError(f"ntbc error {rc}: {_lib.ntbc_last_error().decode()}")
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+class Model:
+    """A model loaded on one device (ntbc_load_model)."""
+
+    def __init__(self, blob: bytes, device: int = 0):
+        self._h = _vp()
+        buf = C.create_string_buffer(blob, len(blob))
+        _check(_lib.ntbc_load_model(buf, len(blob), device, C.byref(self._h)))
+        self.device = device
+        info = _Info()
+        _check(_lib.ntbc_model_get_info(self._h, C.byref(info)))
+        self.n_tex = info.n_textures
+        self.fmts = [info.fmt[i] for i in range(info.n_textures)]
+        self.hidden = info.hidden
+        self.n_e, self.n_c = info.n_endpoint_out, info.n_color_out
+        self.device_bytes = info.device_bytes
+
+    @property
+    def handle(self):
+        return self._h
+
+    def upload_async(self, pinned_blob: torch.Tensor, stream=None):
+        _check(_lib.ntbc_model_upload_async(self._h, pinned_blob.data_ptr(), pinned_blob.numel(), _stream(stream)))
+
+    def free(self):
+        if self._h:
+            _lib.ntbc_free_model(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _handles(models):
+    arr = (_vp * len(models))(*[m.handle.value for m in models])
+    return arr
+
+
+def alloc_outputs(models, width: int, height: int, row_begin: int = 0, row_end: int | None = None, device=None):
+    row_end = height // 4 if row_end is None else row_end
+    dev = torch.device("cuda", models[0].device) if device is None else device
+    n = sum(m.n_tex for m in models)
+    return [torch.empty((row_end - row_begin, width // 4), dtype=torch.int64, device=dev) for _ in range(n)]
+
+
+def decode_material(models, width: int, height: int, outs=None, row_begin: int = 0, row_end: int | None = None,
+                    stream=None):
+    """ntbc_decode_material: returns one int64 [rows][W/4] tensor of BC words per texture."""
+    row_end = height // 4 if row_end is None else row_end
+    if outs is None:
+        outs = alloc_outputs(models, width, height, row_begin, row_end)
+    ptrs = (_vp * len(outs))(*[o.data_ptr() for o in outs])
+    _check(_lib.ntbc_decode_material(_handles(models), len(models), width, height, row_begin, row_end, ptrs,
+                                     _stream(stream)))
+    return outs
+
+
+def decode_material_host(models, pinned_blobs, width: int, height: int, host_outs, stream=None):
+    """ntbc_decode_material_host: pinned host blobs in, pinned host BC words out (async on stream)."""
+    blobs = (_vp * len(models))(*[b.data_ptr() for b in pinned_blobs])
+    sizes = (_sz * len(models))(*[b.numel() for b in pinned_blobs])
+    outs = (_vp * len(host_outs))(*[o.data_ptr() for o in host_outs])
+    _check(_lib.ntbc_decode_material_host(_handles(models), len(models), blobs, sizes, width, height, outs,
+                                          _stream(stream)))
+
+
+def decode_bc(blocks: torch.Tensor, fmt: int, width: int, height: int, out=None, stream=None):
+    ch = 3 if fmt == BC1 else 1
+    if out is None:
+        out = torch.empty((height, width, ch), dtype=torch.float32, device=blocks.device)
+    _check(_lib.ntbc_decode_bc(blocks.data_ptr(), fmt, width, height, out.data_ptr(), _stream(stream)))
+    return out
+
+
+def debug_mlp(model: Model, width: int, height: int, row_begin: int = 0, row_end: int | None = None, stream=None):
+    row_end = height // 4 if row_end is None else row_end
+    rows = row_end - row_begin
+    dev = torch.device("cuda", model.device)
+    ep = torch.empty((rows, width // 4, model.n_e), dtype=torch.float32, device=dev)
+    col = torch.empty((rows * 4, width, model.n_c), dtype=torch.float32, device=dev)
+    _check(_lib.ntbc_debug_mlp(model.handle, width, height, row_begin, row_end, ep.data_ptr(), col.data_ptr(),
+                               _stream(stream)))
+    return ep, col
+
+
+def pack(fmts, endpoints: torch.Tensor, colors: torch.Tensor, width: int, height: int, row_begin: int = 0,
+         row_end: int | None = None, outs=None, stream=None):
+    row_end = height // 4 if row_end is None else row_end
+    if outs is None:
+        outs = [torch.empty((row_end - row_begin, width // 4), dtype=torch.int64, device=endpoints.device)
+                for _ in fmts]
+    f = (C.c_int * len(fmts))(*fmts)
+    ptrs = (_vp * len(outs))(*[o.data_ptr() for o in outs])
+    _check(_lib.ntbc_pack(len(fmts), f, endpoints.data_ptr(), colors.data_ptr(), width, height, row_begin, row_end,
+                          ptrs, _stream(stream)))
+    return outs
+
+
+def debug_mma(A: torch.Tensor, B: torch.Tensor, Cin, K: int, N: int, stream=None):
+    D = torch.empty((128, N), dtype=torch.float32, device=A.device)
+    _check(_lib.ntbc_debug_mma(A.data_ptr(), B.data_ptr(), _ptr(Cin), D.data_ptr(), K, N, _stream(stream)))
+    return D
+
+
+def launch_count() -> int:
+    return int(_lib.ntbc_launch_count())

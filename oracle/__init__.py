@@ -40,6 +40,7 @@ def lib():
             "o_model_info": (None, [vp, vp]),
             "o_f16_to_f32": (f32, [u16]),
             "o_f32_to_f16": (u16, [f32]),
+            "o_f32_to_f16_n": (None, [vp, vp, sz]),
             "o_dequant": (f32, [u8, f32, C.c_int32]),
             "o_exp": (f32, [f32]),
             "o_expm1": (f32, [f32]),
@@ -148,6 +149,13 @@ def decode_bc(blocks: np.ndarray, fmt: int, W: int, H: int) -> np.ndarray:
     b = np.ascontiguousarray(blocks, np.uint64)
     out = np.zeros((H, W, 3 if fmt == BC1 else 1), np.float32)
     lib().o_decode_bc(_p(b), fmt, W, H, _p(out))
+    return out
+
+
+def f32_to_f16(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float32)
+    out = np.zeros(x.shape, np.uint16)
+    lib().o_f32_to_f16_n(_p(x), _p(out), x.size)
     return out
 
 

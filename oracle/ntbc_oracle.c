@@ -145,14 +145,16 @@ uint16_t o_f32_to_f16(float x) {
     uint32_t mant = (uint32_t)fl;
     if (rem > 0.5 || (rem == 0.5 && (mant & 1))) mant++;    /* round half to even */
     /* value = mant * 2^qexp; re-encode */
-    if (qexp == -24) {                                       /* subnormal range (mant <= 1024) */
-        if (mant >= 1024) return (uint16_t)(sign | (1 << 10) | (mant - 1024)); /* rounded up to min normal */
-        return (uint16_t)(sign | mant);
-    }
+    if (qexp == -24)            /* subnormals and the first normal binade share the quantum 2^-24: */
+        return (uint16_t)(sign | mant);   /* bits == mant (mant <= 2048 = 2^-13 after rounding up) */
     int bexp = qexp + 25;                                    /* biased exponent for mant in [1024,2048) */
     if (mant == 2048) { mant = 1024; bexp++; }
     if (bexp >= 31) return (uint16_t)(sign | 0x7c00);
     return (uint16_t)(sign | (bexp << 10) | (mant - 1024));
+}
+
+void o_f32_to_f16_n(const float* x, uint16_t* out, size_t n) {
+    for (size_t i = 0; i < n; i++) out[i] = o_f32_to_f16(x[i]);
 }
 
 /* Eq.2: r = s * (q - z) -- one fp32 multiply of an exact integer (R6) */

@@ -34,6 +34,7 @@ void o_model_info(const o_model* m, int* out16);
 /* ---- scalar building blocks ---- */
 float    o_f16_to_f32(uint16_t h);
 uint16_t o_f32_to_f16(float f);                               /* IEEE RN-even */
+void     o_f32_to_f16_n(const float* x, uint16_t* out, size_t n);
 float    o_dequant(uint8_t q, float s, int32_t z);             /* Eq.2 */
 float    o_exp(float x);                                       /* pinned E, R9 */
 float    o_expm1(float x);                                     /* pinned E-1, R9 */

@@ -41,6 +41,21 @@ def test_f16_to_f32_all_codes_vs_numpy():
     assert np.all(np.isnan(got[np.isnan(ref)]))
 
 
+def test_f32_to_f16_exhaustive_vs_numpy():
+    """Every binary32 value with |x| in [2^-26, 2^17) (all binary16 subnormal, normal and overflow
+    binades, both signs) converts exactly as numpy's IEEE round-to-nearest-even."""
+    lo = np.float32(2.0 ** -26).view(np.uint32)
+    hi = np.float32(2.0 ** 17).view(np.uint32)
+    step = 1 << 24
+    for start in range(int(lo), int(hi), step):
+        bits = np.arange(start, min(start + step, int(hi)), dtype=np.uint32)
+        for sgn in (0, 0x80000000):
+            x = (bits | np.uint32(sgn)).view(np.float32)
+            with np.errstate(over="ignore"):
+                ref = x.astype(np.float16).view(np.uint16)
+            assert np.array_equal(oracle.f32_to_f16(x), ref), hex(start)
+
+
 def test_f32_to_f16_round_nearest_even_vs_numpy():
     rng = np.random.default_rng(1)
     x = np.concatenate([

@@ -79,12 +79,23 @@ def check_material(ntbc, cfg_or_blob, W, H, rows):
     return m, full
 
 
-def test_mma_summation_matches_reading_r10(ntbc):
+@pytest.mark.parametrize("case", ["wide", "subnormal_a", "zero_acc", "cancel"])
+def test_mma_summation_matches_reading_r10(ntbc, case):
     rng = np.random.default_rng(0)
     for K, spread in ((16, 2), (32, 8), (64, 14)):
         A = (np.exp2(rng.uniform(-spread, spread, (128, K))) * rng.choice([-1, 1], (128, K))).astype(np.float16)
         B = (np.exp2(rng.uniform(-spread, spread, (16, K))) * rng.choice([-1, 1], (16, K))).astype(np.float16)
         Cm = (rng.standard_normal((128, 16)) * 4).astype(np.float32)
+        if case == "subnormal_a":     # every activation an fp16 subnormal: R comes from subnormal exponents
+            A = (rng.integers(1, 1024, (128, K)) * 2.0 ** -24 * rng.choice([-1, 1], (128, K))).astype(np.float16)
+        elif case == "zero_acc":      # +0 / -0 accumulators and exactly zero products
+            Cm[::2] = 0.0
+            Cm[1::4] = -0.0
+            A[:, ::3] = 0
+        elif case == "cancel":        # products that cancel exactly to 0 and leave tiny residues
+            B[:, 1::2] = -B[:, 0::2]
+            A[:, 1::2] = A[:, 0::2]
+            A[::2, 0] = np.float16(2.0 ** -20)
         D = ntbc.debug_mma(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), torch.from_numpy(Cm).to(DEV),
                            K, 16).cpu().numpy()
         for i in range(0, 128, 3):
@@ -124,6 +135,16 @@ def test_c1_full_material(ntbc):
 def test_c2_sampled_rows(ntbc):
     W, H, _ = synth.config_shape(2)
     check_material(ntbc, 2, W, H, [(0, 3), (127, 129), (H // 4 - 2, H // 4)])
+
+
+def test_c2_full_material_words(ntbc):
+    """Every BC word of the full 1k material (65,536 blocks x 3 textures) against the oracle."""
+    W, H, _ = synth.config_shape(2)
+    blob = synth.model_blob(2, material=1)
+    outs = ntbc.decode_material([ntbc.Model(blob)], W, H)
+    ref = oracle.Model(blob).decode_material(W, H)
+    for k in range(len(outs)):
+        assert np.array_equal(u64(outs[k]), ref[k]), k
 
 
 @pytest.mark.parametrize("cfg", [3, 4])

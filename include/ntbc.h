@@ -104,6 +104,14 @@ ntbc_status ntbc_decode_bc(const void* blocks, ntbc_format fmt, int width, int h
 ntbc_status ntbc_debug_mlp(ntbc_model m, int width, int height, int row_begin, int row_end,
                            float* endpoints, float* colors, void* stream);
 
+/* Verification only (not timed): rows a1-a2, the fp32 grid features (after Eq.2 dequantization and
+ * bilinear interpolation, before the fp16 rounding of the first MMA operand) of block rows
+ * [row_begin,row_end): block_features: device [rows][width/4][16]; texel_features: device
+ * [rows*4][width][16] (levels coarse->fine x 2 features; unused levels 0).  Written by the same
+ * fused kernel as ntbc_decode_material (dump mode) from the values it feeds the first MMA. */
+ntbc_status ntbc_debug_features(ntbc_model m, int width, int height, int row_begin, int row_end,
+                                float* block_features, float* texel_features, void* stream);
+
 /* Rows a5-a8 as a standalone kernel (quantize + palette + index + pack) fed fp32 MLP outputs in the
  * ntbc_debug_mlp layouts; same output convention as ntbc_decode_material.  fmts: host array of
  * n_textures formats (head order, R17).  Errors: NTBC_EINVAL, NTBC_ECUDA. */

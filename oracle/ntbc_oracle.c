@@ -161,7 +161,7 @@ void o_f32_to_f16_n(const float* x, uint16_t* out, size_t n) {
 float o_dequant(uint8_t q, float s, int32_t z) { return s * (float)((int32_t)q - z); }
 
 /* ------------------------------------------------------------------------- */
-/* pinned exponential E (R9): 2^n * (1 + f*Q(f)), Q a degree-4 polynomial     */
+/* pinned exponential (R9): 2^n * (1 + f*Q(f)), Q a degree-4 polynomial       */
 /* ------------------------------------------------------------------------- */
 static const float LOG2E = 0x1.715476p+0f;
 static const float MAGIC = 12582912.0f;                      /* 1.5 * 2^23 */
@@ -170,25 +170,41 @@ static const float Q0 = 0x1.62e426p-1f, Q1 = 0x1.ebf9b6p-3f, Q2 = 0x1.c6ba7ap-5f
 static const float SELU_L = 0x1.0cfabep+0f;                  /* RN32(1.0507009873554804934) */
 static const float SELU_LA = 0x1.c212ccp+0f;                 /* RN32(lambda * alpha)        */
 
-static void exp_parts(float x, float* s_out, float* u_out) {
-    float xc = fminf(fmaxf(x, -80.0f), 80.0f);
-    float t = xc * LOG2E;
-    float r = t + MAGIC;
-    float nf = r - MAGIC;
-    float f = t - nf;
+/* e^x = 2^n (1 + u): n = rint(x log2e) (magic-number rounding of the exactly-computed product),
+   f = RN(x log2e - n) (exact product, one rounding), u = RN(f Q(f)).  Returns n and u. */
+static int exp_reduce(float x, float* u_out) {
+    float r = fmaf(x, LOG2E, MAGIC);              /* rint(x log2e) + 1.5*2^23, one rounding */
+    float negnf = MAGIC - r;                      /* -n, exact */
+    float f = fmaf(x, LOG2E, negnf);              /* x log2e - n, one rounding */
     float q = fmaf(fmaf(fmaf(fmaf(Q4, f, Q3), f, Q2), f, Q1), f, Q0);
-    float u = f * q;
+    *u_out = f * q;
     int32_t ri, mi; memcpy(&ri, &r, 4); float mg = MAGIC; memcpy(&mi, &mg, 4);
-    int32_t n = ri - mi;
-    uint32_t sb = (uint32_t)(n + 127) << 23;
-    float s; memcpy(&s, &sb, 4);
-    *s_out = s; *u_out = u;
+    return ri - mi;
 }
-float o_exp(float x) { float s, u; exp_parts(x, &s, &u); return fmaf(s, u, s); }
-float o_expm1(float x) { float s, u; exp_parts(x, &s, &u); return fmaf(s, u, s - 1.0f); }
+static float pow2i(int n, float scale) {          /* scale * 2^n by exponent insertion (exact) */
+    uint32_t b; memcpy(&b, &scale, 4);
+    b += (uint32_t)n << 23;
+    float v; memcpy(&v, &b, 4);
+    return v;
+}
+/* E(x) = 2^n + 2^n u, x clamped to [-80, 80] */
+float o_exp(float x) {
+    float xc = fminf(fmaxf(x, -80.0f), 80.0f), u;
+    int n = exp_reduce(xc, &u);
+    float s = pow2i(n, 1.0f);
+    return fmaf(s, u, s);
+}
+/* selu negative branch (R8/R9): lambda*alpha*(e^z - 1) = fma(S, u, S - lambda*alpha), S = lambda*alpha*2^n exact */
+static float selu_neg(float z) {
+    float x = fmaxf(z, -80.0f), u;
+    int n = exp_reduce(x, &u);
+    float S = pow2i(n, SELU_LA);
+    return fmaf(S, u, S - SELU_LA);
+}
+float o_expm1(float x) { return selu_neg(x) / SELU_LA; }   /* for the accuracy pin only (x <= 0) */
 
-/* selu ([selu] Klambauer et al.): lambda*z for z > 0, lambda*alpha*(e^z - 1) otherwise */
-float o_selu(float z) { return z > 0.0f ? SELU_L * z : SELU_LA * o_expm1(z); }
+/* selu ([selu] Klambauer et al.): lambda z (z > 0) else lambda alpha (e^z - 1) */
+float o_selu(float z) { return z > 0.0f ? SELU_L * z : selu_neg(z); }
 /* sigmoid: 1 / (1 + e^-z), IEEE division */
 float o_sigmoid(float z) { float d = 1.0f + o_exp(-z); return 1.0f / d; }
 
@@ -196,8 +212,8 @@ double o_exp_max_relerr(float lo, float hi, int step, int which) {
     double worst = 0.0;
     float x = lo;
     while (x <= hi) {
-        double ref = which == 0 ? exp((double)x) : expm1((double)x);
-        double got = which == 0 ? (double)o_exp(x) : (double)o_expm1(x);
+        double ref = which == 0 ? exp((double)x) : (double)SELU_LA * expm1((double)x);
+        double got = which == 0 ? (double)o_exp(x) : (double)selu_neg(x);
         double den = fabs(ref);
         if (den > 0) { double e = fabs(got - ref) / den; if (e > worst) worst = e; }
         for (int k = 0; k < step; k++) x = nextafterf(x, INFINITY);

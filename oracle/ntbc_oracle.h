@@ -37,7 +37,7 @@ uint16_t o_f32_to_f16(float f);                               /* IEEE RN-even */
 void     o_f32_to_f16_n(const float* x, uint16_t* out, size_t n);
 float    o_dequant(uint8_t q, float s, int32_t z);             /* Eq.2 */
 float    o_exp(float x);                                       /* pinned E, R9 */
-float    o_expm1(float x);                                     /* pinned E-1, R9 */
+float    o_expm1(float x);                                     /* selu_neg(x)/(lambda alpha), accuracy pin only */
 float    o_selu(float z);                                      /* P:333, R8 */
 float    o_sigmoid(float z);                                   /* P:332, R8 */
 
@@ -98,7 +98,7 @@ double   o_block_sq_error(uint64_t blk, int fmt, const float* texels);
 uint64_t o_storage_bytes(int block_levels, int block_coarsest, int texel_levels, int texel_coarsest,
                          int features, int hidden, int n_hidden, int n_e, int n_c, int with_bias);
 
-/* exhaustive accuracy sweep of o_exp / o_expm1 vs libm over [lo,hi], every `step`-th float */
+/* accuracy sweep vs libm over [lo,hi], every `step`-th float: which 0 = E vs exp, 1 = selu's negative branch vs lambda*alpha*expm1 */
 double o_exp_max_relerr(float lo, float hi, int step, int which);
 
 #ifdef __cplusplus

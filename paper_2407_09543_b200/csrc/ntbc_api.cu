@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -233,14 +234,19 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
   p.units_per_row = (p.BW + kUnitBlocks - 1) / kUnitBlocks;
   p.n_units = p.units_per_row * (p.row_end - p.row_begin);
   const int maxo = a.dims[0][4] > a.dims[1][4] ? a.dims[0][4] : a.dims[1][4];
-  const uint32_t a_kmajor = 128u * a.hidden * 2u, a_stage = 128u * 4u * (uint32_t)maxo;
+  const uint32_t a_kmajor = 128u * a.hidden * 2u, a_stage = 128u * 4u * (uint32_t)((maxo + 1) & ~1);  // pairs
   p.a_bytes = (uint32_t)((std::max(a_kmajor, a_stage) + 127) & ~127u);
-  p.pal_bytes = (uint32_t)(a.n_tex * 128 * 32);
+  p.pal_bytes = (uint32_t)(a.n_tex * 128 * (32 + 4));
+  if (const char* e = getenv("NTBC_DEBUG_FLAGS")) p.debug_flags |= (uint32_t)atoi(e);  // 8-float slot + BC header per block and texture
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t cap = 227 * 1024;
-  const int nwg = fused_smem(p, 3) <= cap ? 3 : 2;
+  int nwg = fused_smem(p, 4) <= cap ? 4 : fused_smem(p, 3) <= cap ? 3 : 2;
+  if (const char* e = getenv("NTBC_NWG")) {  // measurement override (bench sweeps); clamped to what fits
+    const int want = atoi(e);
+    if (want >= 2 && want <= 4 && fused_smem(p, want) <= cap) nwg = want;
+  }
   const size_t smem = fused_smem(p, nwg);
   if (smem > cap) return fail(NTBC_EINVAL, "model needs %zu B of shared memory (> %zu)", smem, cap);
   int grid = (p.n_units + nwg - 1) / nwg;
@@ -248,6 +254,8 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
   if (grid < 1) grid = 1;
 #define NTBC_DISPATCH(HH)                                                                        \
   if (a.hidden == HH) {                                                                          \
+    if (nwg == 4) return dump ? launch_fused_t<HH, 4, true>(p, smem, grid, st)                   \
+                              : launch_fused_t<HH, 4, false>(p, smem, grid, st);                 \
     if (nwg == 3) return dump ? launch_fused_t<HH, 3, true>(p, smem, grid, st)                   \
                               : launch_fused_t<HH, 3, false>(p, smem, grid, st);                 \
     return dump ? launch_fused_t<HH, 2, true>(p, smem, grid, st) : launch_fused_t<HH, 2, false>(p, smem, grid, st); \
@@ -425,6 +433,20 @@ ntbc_status ntbc_debug_mlp(ntbc_model m, int width, int height, int r0, int r1, 
   p.W = width; p.H = height; p.row_begin = r0; p.row_end = r1;
   p.dump_ep = endpoints;
   p.dump_col = colors;
+  return launch_fused(m, p, true, (cudaStream_t)stream);
+}
+
+ntbc_status ntbc_debug_features(ntbc_model m, int width, int height, int r0, int r1, float* block_features,
+                                float* texel_features, void* stream) {
+  if (!m || !block_features || !texel_features) return fail(NTBC_EINVAL, "NULL argument");
+  ntbc_status st = check_dims(width, height, r0, r1);
+  if (st) return st;
+  DevGuard dg(m->device);
+  FusedParams p{};
+  p.W = width; p.H = height; p.row_begin = r0; p.row_end = r1;
+  p.dump_ep = block_features;
+  p.dump_col = texel_features;
+  p.debug_flags = 2;
   return launch_fused(m, p, true, (cudaStream_t)stream);
 }
 

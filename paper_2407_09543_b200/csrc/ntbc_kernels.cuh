@@ -46,12 +46,48 @@ struct FusedParams {
   float* dump_ep;   // DUMP mode: [rows][BW][N_e]
   float* dump_col;  // DUMP mode: [rows*4][W][N_c]
   uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
+  uint32_t debug_flags;         // bit 0: scalar grid lookup (A/B checks only)
 };
 
 // ---------------------------------------------------------------- a1-a2: coordinates + grid encode
-// Vertex-centred bilinear lookup of one level (R1), Eq.2 dequantization (R6), lerp = fma(t, b-a, a)
-__device__ __forceinline__ void level_lookup(const uint8_t* blob, const GridLevel& L, float pu, float pv,
-                                             float& f0, float& f1) {
+// Vertex-centred bilinear lookup of one level (R1), Eq.2 dequantization (R6), lerp = fma(t, b-a, a).
+// Both features of a vertex are processed as one fp32x2 pair.  (float)(q - z) is formed exactly as
+// (2^23 + q) - (2^23 + z) from a PRMT-assembled float (Sterbenz), identical to the integer conversion.
+// The reading's clamp i0 = min(floor(X), res-2) never binds here: callers pass p in (0, 1) (rows past
+// the texture edge are clamped to the last valid block/texel), so X = RN(p (res-1)) < res - 1.
+// NOTE: ptxas contracts a mul.rn.f32x2 feeding an add/sub.rn.f32x2 into FFMA2 even with --fmad=false
+// (verified with cuobjdump), which would change the rounding.  Every product that feeds an addition is
+// therefore a scalar __fmul_rn (scalar FMUL -> FADD2 is never contracted); only the lerps are packed.
+__device__ __forceinline__ uint64_t level_lookup2(const uint8_t* blob, const GridLevel& L, float pu, float pv) {
+  const float rm1 = (float)(L.res - 1);
+  const float X = __fmul_rn(pu, rm1), Y = __fmul_rn(pv, rm1);
+  const int i0 = __float2int_rd(X), j0 = __float2int_rd(Y);
+  float fx, fy;
+  f2unpack(sub2(f2pack(X, Y), f2pack((float)i0, (float)j0)), fx, fy);
+  const uint16_t* g = reinterpret_cast<const uint16_t*>(blob + L.offset) + (j0 * L.res + i0);
+  const uint32_t q00 = __ldg(g), q10 = __ldg(g + 1), q01 = __ldg(g + L.res), q11 = __ldg(g + L.res + 1);
+  const float zf = __int_as_float(0x4B000000 + L.z);  // 2^23 + z (z in [0, 255])
+  const uint64_t Z2 = f2pack(zf, zf);
+  float d[8];
+  f2unpack(sub2(f2pack(__int_as_float(__byte_perm(q00, 0x4B000000u, 0x7540)),
+                       __int_as_float(__byte_perm(q00, 0x4B000000u, 0x7541))), Z2), d[0], d[1]);
+  f2unpack(sub2(f2pack(__int_as_float(__byte_perm(q10, 0x4B000000u, 0x7540)),
+                       __int_as_float(__byte_perm(q10, 0x4B000000u, 0x7541))), Z2), d[2], d[3]);
+  f2unpack(sub2(f2pack(__int_as_float(__byte_perm(q01, 0x4B000000u, 0x7540)),
+                       __int_as_float(__byte_perm(q01, 0x4B000000u, 0x7541))), Z2), d[4], d[5]);
+  f2unpack(sub2(f2pack(__int_as_float(__byte_perm(q11, 0x4B000000u, 0x7540)),
+                       __int_as_float(__byte_perm(q11, 0x4B000000u, 0x7541))), Z2), d[6], d[7]);
+  const uint64_t v00 = f2pack(__fmul_rn(L.s, d[0]), __fmul_rn(L.s, d[1]));
+  const uint64_t v10 = f2pack(__fmul_rn(L.s, d[2]), __fmul_rn(L.s, d[3]));
+  const uint64_t v01 = f2pack(__fmul_rn(L.s, d[4]), __fmul_rn(L.s, d[5]));
+  const uint64_t v11 = f2pack(__fmul_rn(L.s, d[6]), __fmul_rn(L.s, d[7]));
+  const uint64_t FX = f2pack(fx, fx), FY = f2pack(fy, fy);
+  const uint64_t top = fma2(FX, sub2(v10, v00), v00), bot = fma2(FX, sub2(v11, v01), v01);
+  return fma2(FY, sub2(bot, top), top);
+}
+
+__device__ __forceinline__ void level_lookup_scalar(const uint8_t* blob, const GridLevel& L, float pu, float pv,
+                                                    float& f0, float& f1) {
   const float rm1 = (float)(L.res - 1);
   const float X = __fmul_rn(pu, rm1), Y = __fmul_rn(pv, rm1);
   int i0 = (int)floorf(X), j0 = (int)floorf(Y);
@@ -78,12 +114,16 @@ __device__ __forceinline__ void level_lookup(const uint8_t* blob, const GridLeve
 // 16 features (levels coarse->fine, 2 per level, R3) of grid g at (pu, pv), rounded to fp16 and
 // written as row `row` of a K-major [128][K] operand (columns 0..15; unused levels are zero).
 __device__ __forceinline__ void write_feature_row(const FusedParams& p, int g, float pu, float pv, uint8_t* A,
-                                                  int row, int K) {
+                                                  int row, int K, float* dump = nullptr) {
   uint32_t h[8];
 #pragma unroll
   for (int l = 0; l < kMaxLevels; l++) {
     float f0 = 0.0f, f1 = 0.0f;
-    if (l < p.levels[g]) level_lookup(p.blob, p.lv[g][l], pu, pv, f0, f1);
+    if (l < p.levels[g]) {
+      if (p.debug_flags & 1) level_lookup_scalar(p.blob, p.lv[g][l], pu, pv, f0, f1);
+      else f2unpack(level_lookup2(p.blob, p.lv[g][l], pu, pv), f0, f1);
+    }
+    if (dump) { dump[2 * l] = f0; dump[2 * l + 1] = f1; }
     const __half2 v = __floats2half2_rn(f0, f1);
     h[l] = *reinterpret_cast<const uint32_t*>(&v);
   }
@@ -98,6 +138,21 @@ __device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* r) {
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t& a, uint32_t& b) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a), "+r"(b)::"memory");
+}
+
+// tcgen05.wait::ld that also "touches" the 16 destination registers, so the compiler cannot move their
+// uses above the wait (the registers are undefined until the asynchronous load completes).
+__device__ __forceinline__ void tmem_wait_ld16(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
 }
 
 // Issue one layer of the MLP for the 128 rows of a work group (called by ONE thread):
@@ -130,6 +185,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   uint8_t* A = wg_base;                                           // [128][H] K-major fp16 / fp32 staging
   float* stage = reinterpret_cast<float*>(A);                     // [ch][128] fp32 (after the last MMA)
   float* pal = reinterpret_cast<float*>(wg_base + p.a_bytes);     // [tex][128 blocks][8] fp32
+  uint32_t* hdrs = reinterpret_cast<uint32_t*>(pal + p.n_tex * 128 * 8);  // [tex][128 blocks] BC word low bits
   uint64_t* bars = reinterpret_cast<uint64_t*>(ones + 4096 + NWG * (p.a_bytes + p.pal_bytes));
   uint64_t* bar_w = bars;                                         // weights landed
   uint64_t* bar_mma = bars + 1 + wg;                              // this work group's MMA completion
@@ -184,39 +240,34 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       mbar_wait(bar_mma, phase);
       phase ^= 1u;
       tc_fence_after();
-      if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10)
-        uint32_t acc[H];
+      if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10), 16 columns at a time
+        uint32_t buf[2][16];
+        tmem_ld16p(tm_row, buf[0]);
+        tmem_wait_ld16(buf[0]);
 #pragma unroll
-        for (int c = 0; c < H / 16; c++) tmem_ld16p(tm_row + c * 16, acc + c * 16);
-        tmem_wait_ld();
+        for (int c = 0; c < H / 16; c++) {
+          if (c + 1 < H / 16) tmem_ld16p(tm_row + (c + 1) * 16, buf[(c + 1) & 1]);   // prefetch next chunk
+          uint32_t hv[8];
 #pragma unroll
-        for (int k8 = 0; k8 < H / 8; k8++) {
-          uint32_t hv[4];
-#pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const float a = selu(__uint_as_float(acc[k8 * 8 + 2 * j]));
-            const float b = selu(__uint_as_float(acc[k8 * 8 + 2 * j + 1]));
-            const __half2 v = __floats2half2_rn(a, b);
-            hv[j] = *reinterpret_cast<const uint32_t*>(&v);
-          }
-          *reinterpret_cast<uint4*>(A + kmajor_offset(r, k8 * 8, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+          for (int j = 0; j < 8; j++)
+            hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
+          *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+          *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+          if (c + 1 < H / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
         }
       }
     }
   };
-  // output layer epilogue: sigmoid of the n_out columns -> fp32 staging [ch][128] (own row only)
+  // output layer epilogue: sigmoid of the n_out columns (pairs, rounded up) -> fp32 staging [ch][128]
   auto stage_outputs = [&](int n) {
-    uint32_t acc[48];  // n_out16 <= 48 is enforced at load
-    const int n16 = p.net[n].n_out16;
-#pragma unroll
-    for (int c = 0; c < 3; c++)
-      if (c * 16 < n16) tmem_ld16p(tm_row + c * 16, acc + c * 16);
-    tmem_wait_ld();
-    // the output MMA has completed (mbarrier), so A may be overwritten by the fp32 staging
     const int no = p.net[n].n_out;
-#pragma unroll
-    for (int ch = 0; ch < 48; ch++)
-      if (ch < no) stage[ch * 128 + r] = sigmoid(__uint_as_float(acc[ch]));
+#pragma unroll 1
+    for (int ch = 0; ch < no; ch += 2) {
+      uint32_t a, b;
+      tmem_ld2(tm_row + ch, a, b);
+      stage[ch * 128 + r] = sigmoid(__uint_as_float(a));
+      stage[(ch + 1) * 128 + r] = sigmoid(__uint_as_float(b));
+    }
   };
 
 #pragma unroll 1
@@ -229,33 +280,37 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     // ================= endpoint tile: row r = block (bx0 + r, by)  (rows a1-a3, a5-a6)
     named_bar_sync(bar_id, 128);  // previous tile's readers of A / staging / palettes are done
     {
-      const float s = __fdiv_rn(__fadd_rn((float)(bx0 + r), 0.5f), (float)p.BW);
+      const float s = __fdiv_rn(__fadd_rn((float)min(bx0 + r, p.BW - 1), 0.5f), (float)p.BW);
       const float t = __fdiv_rn(__fadd_rn((float)by, 0.5f), (float)p.BH);
-      write_feature_row(p, 0, s, t, A, r, H);
+      float* fd = (DUMP && (p.debug_flags & 2) && r < nvalid) ? p.dump_ep + (out_row + bx0 + r) * 16 : nullptr;
+      write_feature_row(p, 0, s, t, A, r, H, fd);
     }
     run_mlp(0);
     stage_outputs(0);
     if (DUMP) {
-      if (r < nvalid)
+      if (r < nvalid && !(p.debug_flags & 2))
         for (int ch = 0; ch < p.net[0].n_out; ch++)
           p.dump_ep[(out_row + bx0 + r) * p.net[0].n_out + ch] = stage[ch * 128 + r];
     } else {
       for (int k = 0; k < p.n_tex; k++) {
         const int eo = p.ep_off[k];
         float4* slot = reinterpret_cast<float4*>(pal + ((size_t)k * 128 + r) * 8);
-        if (p.fmt[k] == kFmtBC1) {
+        if (p.fmt[k] == kFmtBC1) {  // slot = quantized endpoints e0q, e1q (R11, R12)
           float ep[6], e0[3], e1[3];
 #pragma unroll
           for (int c = 0; c < 6; c++) ep[c] = stage[(eo + c) * 128 + r];
-          const uint32_t hdr = quant_bc1(ep, e0, e1);
+          hdrs[k * 128 + r] = quant_bc1(ep, e0, e1);
           slot[0] = make_float4(e0[0], e0[1], e0[2], e1[0]);
-          slot[1] = make_float4(e1[1], e1[2], __uint_as_float(hdr), 0.0f);
-        } else {
-          float ep[2], e0, e1;
+          slot[1] = make_float4(e1[1], e1[2], 0.0f, 0.0f);
+        } else {                    // slot = the full 8-entry linear palette (Eq.7/8, R13, R18)
+          float ep[2], e0, e1, pl[8];
           ep[0] = stage[eo * 128 + r];
           ep[1] = stage[(eo + 1) * 128 + r];
           const uint32_t hdr = quant_bc4(ep, e0, e1);
-          slot[0] = make_float4(e0, e1, __uint_as_float(hdr), 0.0f);
+          hdrs[k * 128 + r] = hdr;
+          bc4_palette(hdr, pl);
+          slot[0] = make_float4(pl[0], pl[1], pl[2], pl[3]);
+          slot[1] = make_float4(pl[4], pl[5], pl[6], pl[7]);
         }
       }
     }
@@ -264,35 +319,37 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
 #pragma unroll 1
     for (int j = 0; j < kUnitBlocks / 8 && 8 * j < nvalid; j++) {
       const int b = 8 * j + (r >> 4), i = r & 15;
-      const int bx = bx0 + b, x = 4 * bx + (i & 3), y = 4 * by + (i >> 2);
+      const int bx = bx0 + b, x = 4 * min(bx, p.BW - 1) + (i & 3), y = 4 * by + (i >> 2);
       named_bar_sync(bar_id, 128);
       {
         const float pu = __fdiv_rn(__fadd_rn((float)x, 0.5f), (float)p.W);
         const float pv = __fdiv_rn(__fadd_rn((float)y, 0.5f), (float)p.H);
-        write_feature_row(p, 1, pu, pv, A, r, H);
+        float* fd = (DUMP && (p.debug_flags & 2) && b < nvalid)
+                        ? p.dump_col + (((size_t)(y - 4 * p.row_begin)) * p.W + x) * 16 : nullptr;
+        write_feature_row(p, 1, pu, pv, A, r, H, fd);
       }
       run_mlp(1);
       stage_outputs(1);
       if (DUMP) {
-        if (b < nvalid)
+        if (b < nvalid && !(p.debug_flags & 2))
           for (int ch = 0; ch < p.net[1].n_out; ch++)
             p.dump_col[(((size_t)(y - 4 * p.row_begin)) * p.W + x) * p.net[1].n_out + ch] = stage[ch * 128 + r];
       } else {
         for (int k = 0; k < p.n_tex; k++) {
           const int co = p.col_off[k];
           const float4* slot = reinterpret_cast<const float4*>(pal + ((size_t)k * 128 + b) * 8);
+          const uint32_t hdr = hdrs[k * 128 + b];
           uint64_t word;
           if (p.fmt[k] == kFmtBC1) {
             const float4 s0 = slot[0], s1 = slot[1];
             const float e0[3] = {s0.x, s0.y, s0.z}, e1[3] = {s0.w, s1.x, s1.y};
-            const uint32_t hdr = __float_as_uint(s1.z);
             const float c[3] = {stage[co * 128 + r], stage[(co + 1) * 128 + r], stage[(co + 2) * 128 + r]};
             const uint32_t code = bc1_code(c, e0, e1, (hdr & 0xFFFFu) == (hdr >> 16));
             word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
           } else {
-            const float4 s0 = slot[0];
-            const uint32_t hdr = __float_as_uint(s0.z);
-            const uint32_t code = bc4_code(stage[co * 128 + r], s0.x, s0.y, (hdr & 0xFFu) > (hdr >> 8));
+            const float4 s0 = slot[0], s1 = slot[1];
+            const float pl[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            const uint32_t code = bc4_code(stage[co * 128 + r], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu));
             word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
           }
           if ((lane & 15) == 0 && b < nvalid) p.out[k][out_row + bx] = word;
@@ -342,7 +399,9 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
         ep[0] = __ldg(e + p.ep_off[k]);
         ep[1] = __ldg(e + p.ep_off[k] + 1);
         const uint32_t hdr = quant_bc4(ep, e0, e1);
-        const uint32_t code = bc4_code(__ldg(c + p.col_off[k]), e0, e1, (hdr & 0xFFu) > (hdr >> 8));
+        float pl[8];
+        bc4_palette(hdr, pl);
+        const uint32_t code = bc4_code(__ldg(c + p.col_off[k]), pl, (hdr & 0xFFu) > (hdr >> 8));
         word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
       }
       if ((lane & 15) == 0 && valid) p.out[k][(size_t)row * p.BW + bx] = word;
@@ -367,35 +426,30 @@ __global__ void __launch_bounds__(256) decode_bc_kernel(const uint64_t* __restri
       e0[2] = __fdiv_rn((float)(c0 & 31), 31.0f);
       e1[0] = __fdiv_rn((float)(c1 >> 11), 31.0f); e1[1] = __fdiv_rn((float)((c1 >> 5) & 63), 63.0f);
       e1[2] = __fdiv_rn((float)(c1 & 31), 31.0f);
+      // 4-colour mode: code -> linear n = [0,3,1,2] -> weights n/3 (R18)
+      const int n_lin = (0x2130 >> (4 * code)) & 3;
+      const float w = n_lin == 0 ? 0.0f : n_lin == 1 ? NTBC_W3_1 : n_lin == 2 ? NTBC_W3_2 : 1.0f;
+      const float wb = n_lin == 0 ? 1.0f : n_lin == 1 ? NTBC_WB3_1 : n_lin == 2 ? NTBC_WB3_2 : 0.0f;
       float v[3];
 #pragma unroll
       for (int ch = 0; ch < 3; ch++) {
-        if (c0 > c1) {  // 4-colour mode: code -> linear n = [0,3,1,2]
-          const int n_lin = (0x2130 >> (4 * code)) & 3;
-          const float w = __fdiv_rn((float)n_lin, 3.0f);
-          v[ch] = interp(w, e0[ch], e1[ch]);
-        } else {        // DirectX 3-colour mode (never emitted by the encoder, R12)
+        if (c0 > c1) v[ch] = interp_c(w, wb, e0[ch], e1[ch]);
+        else  // DirectX 3-colour mode (never emitted by the encoder, R12)
           v[ch] = code == 0 ? e0[ch] : code == 1 ? e1[ch] : code == 2 ? __fmaf_rn(0.5f, e1[ch], __fmul_rn(0.5f, e0[ch])) : 0.0f;
-        }
       }
       float* o = out + (size_t)t * 3;
       o[0] = v[0]; o[1] = v[1]; o[2] = v[2];
     } else {
       const uint32_t E0 = (uint32_t)(blk & 0xFF), E1 = (uint32_t)((blk >> 8) & 0xFF);
       const uint32_t code = (uint32_t)(blk >> (16 + 3 * i)) & 7u;
-      const float e0 = __fdiv_rn((float)E0, 255.0f), e1 = __fdiv_rn((float)E1, 255.0f);
-      float v;
-      if (E0 > E1) {  // code -> linear n: 0->0, 1->7, c->c-1
-        const int n_lin = code == 0 ? 0 : code == 1 ? 7 : (int)code - 1;
-        v = interp(__fdiv_rn((float)n_lin, 7.0f), e0, e1);
-      } else {        // code -> linear n: 0->1, 1->6, 2..5->same, 6->0 (0.0), 7->7 (1.0)
-        if (code == 6) v = 0.0f;
-        else if (code == 7) v = 1.0f;
-        else {
-          const int n_lin = code == 0 ? 1 : code == 1 ? 6 : (int)code;
-          v = interp(__fdiv_rn((float)(n_lin - 1), 5.0f), e0, e1);
-        }
-      }
+      float pl[8];
+      bc4_palette(E0 | (E1 << 8), pl);
+      // code -> linear n: mode8 0->0, 1->7, c->c-1; mode6 0->1, 1->6, 2..5->same, 6->0, 7->7
+      const int n_lin = E0 > E1 ? (code == 0 ? 0 : code == 1 ? 7 : (int)code - 1)
+                                : (code == 0 ? 1 : code == 1 ? 6 : code == 6 ? 0 : (int)code);
+      float v = pl[0];
+#pragma unroll
+      for (int n = 1; n < 8; n++) v = n_lin == n ? pl[n] : v;
       out[t] = v;
     }
   }
@@ -460,7 +514,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(const __half* __restr
   for (int c = 0; c < N; c += 16) {
     uint32_t v[16];
     tmem_ld16p(trow + c, v);
-    tmem_wait_ld();
+    tmem_wait_ld16(v);
 #pragma unroll
     for (int j = 0; j < 16; j++) D[(size_t)r * N + c + j] = __uint_as_float(v[j]);
   }

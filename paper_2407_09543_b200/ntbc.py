@@ -40,6 +40,7 @@ _SIGS = {
     "ntbc_decode_material_host": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _vp]),
     "ntbc_decode_bc": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "ntbc_debug_mlp": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
+    "ntbc_debug_features": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ntbc_pack": (_i, [_i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "ntbc_debug_mma": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp]),
     "ntbc_launch_count": (C.c_uint64, []),
@@ -157,6 +158,19 @@ def debug_mlp(model: Model, width: int, height: int, row_begin: int = 0, row_end
     _check(_lib.ntbc_debug_mlp(model.handle, width, height, row_begin, row_end, ep.data_ptr(), col.data_ptr(),
                                _stream(stream)))
     return ep, col
+
+
+def debug_features(model: Model, width: int, height: int, row_begin: int = 0, row_end: int | None = None,
+                   stream=None):
+    """fp32 grid features (16 per block / texel) of block rows [row_begin, row_end)."""
+    row_end = height // 4 if row_end is None else row_end
+    rows = row_end - row_begin
+    dev = torch.device("cuda", model.device)
+    bf = torch.zeros((rows, width // 4, 16), dtype=torch.float32, device=dev)
+    tf = torch.zeros((rows * 4, width, 16), dtype=torch.float32, device=dev)
+    _check(_lib.ntbc_debug_features(model.handle, width, height, row_begin, row_end, bf.data_ptr(), tf.data_ptr(),
+                                    _stream(stream)))
+    return bf, tf
 
 
 def pack(fmts, endpoints: torch.Tensor, colors: torch.Tensor, width: int, height: int, row_begin: int = 0,

@@ -127,6 +127,33 @@ def test_pack_bit_exact(ntbc, fmts, BW, BH):
         assert np.array_equal(u64(g[k]), o[k]), k
 
 
+@pytest.mark.parametrize("cfg,rows", [(1, (0, 16)), (2, (0, 2)), (3, (511, 512)), (4, (1023, 1024))])
+def test_grid_features_bit_exact(ntbc, cfg, rows):
+    """Rows a1-a2 in isolation: Eq.2 dequantization + vertex-centred bilinear sampling, every feature of
+    every block and texel of the sampled rows, bit-exact (R1-R3, R6)."""
+    W, H, _ = synth.config_shape(cfg)
+    blob = synth.model_blob(cfg)
+    m, om = ntbc.Model(blob), oracle.Model(blob)
+    bf, tf = ntbc.debug_features(m, W, H, *rows)
+    bf, tf = bf.cpu().numpy(), tf.cpu().numpy()
+    r0, r1 = rows
+    nb, nt = 2 * om.block_levels, 2 * om.texel_levels
+    f32 = np.float32
+    for r in range(r1 - r0):
+        by = r0 + r
+        t = f32((f32(by) + f32(0.5)) / f32(H // 4))
+        for bx in range(0, W // 4, max(1, W // 4 // 256)):
+            s_ = f32((f32(bx) + f32(0.5)) / f32(W // 4))
+            assert np.array_equal(bf[r, bx, :nb].view(np.uint32), om.grid_encode(0, float(s_), float(t)).view(np.uint32))
+        for yy in range(4):
+            y = 4 * by + yy
+            v = f32((f32(y) + f32(0.5)) / f32(H))
+            for x in range(0, W, max(1, W // 1024)):
+                u = f32((f32(x) + f32(0.5)) / f32(W))
+                got = tf[4 * r + yy, x, :nt]
+                assert np.array_equal(got.view(np.uint32), om.grid_encode(1, float(u), float(v)).view(np.uint32)), (x, y)
+
+
 def test_c1_full_material(ntbc):
     W, H, _ = synth.config_shape(1)
     check_material(ntbc, 1, W, H, [(0, H // 4)])

@@ -86,9 +86,9 @@ def test_dequant_eq2_single_rounding():
 # ---------------------------------------------------------------- pinned exp (R9), selu / sigmoid
 def test_exp_accuracy_vs_libm():
     assert L.o_exp(0.0) == 1.0
-    assert L.o_exp_max_relerr(-80.0, 80.0, 100003, 0) < 4e-6      # t = x*log2e rounding dominates
-    assert L.o_exp_max_relerr(-10.0, 10.0, 10007, 0) < 1e-6
-    assert L.o_exp_max_relerr(-20.0, -1e-30, 20011, 1) < 1e-6      # expm1 on the selu branch
+    assert L.o_exp_max_relerr(-80.0, 80.0, 100003, 0) < 2e-6
+    assert L.o_exp_max_relerr(-10.0, 10.0, 10007, 0) < 5e-7
+    assert L.o_exp_max_relerr(-80.0, -1e-30, 20011, 1) < 1e-6      # selu's lambda*alpha*(e^z - 1) branch
     assert L.o_exp_max_relerr(-1e-2, -1e-30, 1009, 1) < 1e-6       # no cancellation near 0^-
 
 

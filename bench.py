@@ -171,6 +171,7 @@ def run_ours(args, rank, world, local_rank):
 
     import synth
     from paper_2407_09543_b200 import ntbc
+    from paper_2407_09543_b200.shard import gather_materials
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -182,14 +183,13 @@ def run_ours(args, rank, world, local_rank):
     plane = BH * BW
     out_all = torch.empty((n_tex, BH, BW), dtype=torch.int64, device=dev)   # contiguous for the gather
     outs = [out_all[k] for k in range(n_tex)]
-    gather = [torch.empty_like(out_all) for _ in range(world)] if (world > 1 and rank == 0) else None
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step():
         ntbc.decode_material([model], W, H, outs=outs, stream=stream)
-        if world > 1:
-            dist.gather(out_all, gather if rank == 0 else None, dst=0)
+        if world > 1:   # the final gather of packed bytes to rank 0 (north star), inside the timed step
+            gather_materials(out_all, rank, world)
 
     for _ in range(max(args.warmup, 3)):
         step()

@@ -208,6 +208,7 @@ size_t fused_smem(const FusedParams& p, int nwg) {
 ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
   const Arch& a = m->arch;
   p.blob = m->d_blob;
+  p.k23 = 1 << 23;
   p.img = m->d_img;
   for (int g = 0; g < 2; g++) {
     p.levels[g] = a.levels[g];

@@ -46,7 +46,8 @@ struct FusedParams {
   float* dump_ep;   // DUMP mode: [rows][BW][N_e]
   float* dump_col;  // DUMP mode: [rows*4][W][N_c]
   uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
-  uint32_t debug_flags;         // bit 0: scalar grid lookup (A/B checks only)
+  uint32_t debug_flags;         // bit 0: scalar grid lookup (A/B checks only); bit 1: feature dump
+  int k23;                      // = 1 << 23 (run-time constant, see selu2_h2)
 };
 
 // ---------------------------------------------------------------- a1-a2: coordinates + grid encode
@@ -237,7 +238,8 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
         issue_layer(tm, a_base, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
         mma_commit(bar_mma);
       }
-      mbar_wait(bar_mma, phase);
+      if (r == 0) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
+      named_bar_sync(bar_id, 128);
       phase ^= 1u;
       tc_fence_after();
       if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10), 16 columns at a time
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           uint32_t hv[8];
 #pragma unroll
           for (int j = 0; j < 8; j++)
-            hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
+            hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]), p.k23);
           *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
           *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
           if (c + 1 < H / 16) tmem_wait_ld16(buf[(c + 1) & 1]);

@@ -238,7 +238,6 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
   const uint32_t a_kmajor = 128u * a.hidden * 2u, a_stage = 128u * 4u * (uint32_t)((maxo + 1) & ~1);  // pairs
   p.a_bytes = (uint32_t)((std::max(a_kmajor, a_stage) + 127) & ~127u);
   p.pal_bytes = (uint32_t)(a.n_tex * 128 * (32 + 4));
-  if (const char* e = getenv("NTBC_DEBUG_FLAGS")) p.debug_flags |= (uint32_t)atoi(e);  // 8-float slot + BC header per block and texture
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

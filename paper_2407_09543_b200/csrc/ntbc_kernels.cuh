@@ -46,7 +46,7 @@ struct FusedParams {
   float* dump_ep;   // DUMP mode: [rows][BW][N_e]
   float* dump_col;  // DUMP mode: [rows*4][W][N_c]
   uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
-  uint32_t debug_flags;         // bit 0: scalar grid lookup (A/B checks only); bit 1: feature dump
+  uint32_t debug_flags;         // bit 1: grid-feature dump (ntbc_debug_features)
   int k23;                      // = 1 << 23 (run-time constant, see selu2_h2)
 };
 
@@ -87,31 +87,6 @@ __device__ __forceinline__ uint64_t level_lookup2(const uint8_t* blob, const Gri
   return fma2(FY, sub2(bot, top), top);
 }
 
-__device__ __forceinline__ void level_lookup_scalar(const uint8_t* blob, const GridLevel& L, float pu, float pv,
-                                                    float& f0, float& f1) {
-  const float rm1 = (float)(L.res - 1);
-  const float X = __fmul_rn(pu, rm1), Y = __fmul_rn(pv, rm1);
-  int i0 = (int)floorf(X), j0 = (int)floorf(Y);
-  i0 = max(0, min(i0, L.res - 2));
-  j0 = max(0, min(j0, L.res - 2));
-  const float fx = __fsub_rn(X, (float)i0), fy = __fsub_rn(Y, (float)j0);
-  const uint16_t* g = reinterpret_cast<const uint16_t*>(blob + L.offset);
-  const uint32_t q00 = __ldg(g + j0 * L.res + i0), q10 = __ldg(g + j0 * L.res + i0 + 1);
-  const uint32_t q01 = __ldg(g + (j0 + 1) * L.res + i0), q11 = __ldg(g + (j0 + 1) * L.res + i0 + 1);
-#define NTBC_DQ(q, sh) __fmul_rn(L.s, (float)((int)(((q) >> (sh)) & 0xFFu) - L.z))
-#define NTBC_LERP(a, b, t) __fmaf_rn((t), __fsub_rn((b), (a)), (a))
-  {
-    const float v00 = NTBC_DQ(q00, 0), v10 = NTBC_DQ(q10, 0), v01 = NTBC_DQ(q01, 0), v11 = NTBC_DQ(q11, 0);
-    f0 = NTBC_LERP(NTBC_LERP(v00, v10, fx), NTBC_LERP(v01, v11, fx), fy);
-  }
-  {
-    const float v00 = NTBC_DQ(q00, 8), v10 = NTBC_DQ(q10, 8), v01 = NTBC_DQ(q01, 8), v11 = NTBC_DQ(q11, 8);
-    f1 = NTBC_LERP(NTBC_LERP(v00, v10, fx), NTBC_LERP(v01, v11, fx), fy);
-  }
-#undef NTBC_DQ
-#undef NTBC_LERP
-}
-
 // 16 features (levels coarse->fine, 2 per level, R3) of grid g at (pu, pv), rounded to fp16 and
 // written as row `row` of a K-major [128][K] operand (columns 0..15; unused levels are zero).
 __device__ __forceinline__ void write_feature_row(const FusedParams& p, int g, float pu, float pv, uint8_t* A,
@@ -120,10 +95,7 @@ __device__ __forceinline__ void write_feature_row(const FusedParams& p, int g, f
 #pragma unroll
   for (int l = 0; l < kMaxLevels; l++) {
     float f0 = 0.0f, f1 = 0.0f;
-    if (l < p.levels[g]) {
-      if (p.debug_flags & 1) level_lookup_scalar(p.blob, p.lv[g][l], pu, pv, f0, f1);
-      else f2unpack(level_lookup2(p.blob, p.lv[g][l], pu, pv), f0, f1);
-    }
+    if (l < p.levels[g]) f2unpack(level_lookup2(p.blob, p.lv[g][l], pu, pv), f0, f1);
     if (dump) { dump[2 * l] = f0; dump[2 * l + 1] = f1; }
     const __half2 v = __floats2half2_rn(f0, f1);
     h[l] = *reinterpret_cast<const uint32_t*>(&v);

@@ -60,8 +60,9 @@ def main(rep, tag, config=3, texels=4096 * 4096):
     out["warp_instructions"] = total
     out["thread_instructions_per_texel"] = total * 32 / texels
     out["op_mix_per_texel"] = {k: round(v * 32 / texels, 1) for k, v in ops.most_common(25)}
-    rd = float(m["dram__bytes_read.sum"][0]) * (1e6 if m["dram__bytes_read.sum"][1] == "Mbyte" else 1)
-    wr = float(m["dram__bytes_write.sum"][0]) * (1e6 if m["dram__bytes_write.sum"][1] == "Mbyte" else 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rd = float(m["dram__bytes_read.sum"][0]) * scale[m["dram__bytes_read.sum"][1]]
+    wr = float(m["dram__bytes_write.sum"][0]) * scale[m["dram__bytes_write.sum"][1]]
     out["dram_bytes_per_launch"] = rd + wr
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_fused_ncu.json"), "w") as f:

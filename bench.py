@@ -118,12 +118,13 @@ def oracle_sample(cfg: int, budget_s: float = 15.0, material: int = 0):
     W, H, spec = synth.config_shape(cfg)
     om = oracle.Model(synth.model_blob(cfg, material))
     threads = os.cpu_count() or 1
+    om.decode_material(W, H, 0, 1, nthreads=threads)          # warm-up (thread pool, page-in)
     t0 = time.perf_counter()
-    om.decode_material(W, H, 0, 1, nthreads=threads)
-    t_row = time.perf_counter() - t0
-    rows = int(max(1, min(H // 4 - 1, budget_s / max(t_row, 1e-3))))
+    om.decode_material(W, H, 1, 3, nthreads=threads)          # estimate the per-row cost
+    t_row = (time.perf_counter() - t0) / 2
+    rows = int(max(1, min(H // 4 - 3, budget_s / max(t_row, 1e-3))))
     t0 = time.perf_counter()
-    om.decode_material(W, H, 1, 1 + rows, nthreads=threads)
+    om.decode_material(W, H, 3, 3 + rows, nthreads=threads)
     dt = time.perf_counter() - t0
     blocks = rows * (W // 4) * len(spec.fmts)
     return {"value": blocks / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",

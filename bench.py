@@ -119,12 +119,14 @@ def oracle_sample(cfg: int, budget_s: float = 15.0, material: int = 0):
     om = oracle.Model(synth.model_blob(cfg, material))
     threads = os.cpu_count() or 1
     om.decode_material(W, H, 0, 1, nthreads=threads)          # warm-up (thread pool, page-in)
+    est = max(1, min(threads, H // 8))                        # the oracle parallelises over rows: estimate
+    t0 = time.perf_counter()                                  # the per-row cost with every thread busy
+    om.decode_material(W, H, 1, 1 + est, nthreads=threads)
+    t_row = (time.perf_counter() - t0) / est
+    r0 = 1 + est
+    rows = int(max(1, min(H // 4 - r0, budget_s / max(t_row, 1e-3))))
     t0 = time.perf_counter()
-    om.decode_material(W, H, 1, 3, nthreads=threads)          # estimate the per-row cost
-    t_row = (time.perf_counter() - t0) / 2
-    rows = int(max(1, min(H // 4 - 3, budget_s / max(t_row, 1e-3))))
-    t0 = time.perf_counter()
-    om.decode_material(W, H, 3, 3 + rows, nthreads=threads)
+    om.decode_material(W, H, r0, r0 + rows, nthreads=threads)
     dt = time.perf_counter() - t0
     blocks = rows * (W // 4) * len(spec.fmts)
     return {"value": blocks / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
@@ -232,14 +234,16 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(2):
         ntbc.decode_material_host([model], [pinned_blob], W, H, host_out, stream=stream)
     torch.cuda.synchronize()
+    # consecutive calls pipeline (the next material's upload overlaps the current decode, copy-back
+    # overlaps the kernel), so time the whole span of e_steps calls on the device, not per call
     e_steps = max(3, min(args.steps, 20))
-    eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e_steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
     for s in range(e_steps):
-        eev[s][0].record(stream)
         ntbc.decode_material_host([model], [pinned_blob], W, H, host_out, stream=stream)
-        eev[s][1].record(stream)
+    e1.record(stream)
     torch.cuda.synchronize()
-    e_ms = sum(a.elapsed_time(b) for a, b in eev) / e_steps
+    e_ms = e0.elapsed_time(e1) / e_steps
     e_tensor = torch.tensor([e_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e_tensor, op=dist.ReduceOp.MAX)

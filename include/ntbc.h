@@ -87,6 +87,14 @@ ntbc_status ntbc_decode_material(const ntbc_model* models, int n_models, int wid
  * and copies every texture's BC words device->host into host_out[t] (height/4 * width/4 * 8 bytes).
  * Uses model-owned device scratch (allocated on first use for a given size, outside any timed loop).
  * Asynchronous on `stream`; call cudaStreamSynchronize before reading host_out.
+ * Pipelining (when the device supports 64-bit stream memory operations; NTBC_NO_PIPELINED_COPY=1
+ * disables it): the blob is uploaded into the model's idle second weight slot on an internal stream
+ * that does NOT wait for earlier work on `stream` -- the blob must hold its final contents when this
+ * function is called and stay unchanged until `stream` reaches this call -- so the upload overlaps the
+ * previous call's kernel; the kernel publishes finished row chunks (1/16 of the rows each) through
+ * device counters and an internal copy stream copies each chunk back while later rows are decoded.
+ * `stream` waits for all of it, so host_out is complete once `stream` reaches this call.
+ * Not re-entrant per model: calls on the same model must not run concurrently on different streams.
  * Errors: as ntbc_decode_material, plus NTBC_ENOMEM. */
 ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, const void* const* blobs,
                                       const size_t* blob_sizes, int width, int height,

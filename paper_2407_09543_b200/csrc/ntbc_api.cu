@@ -1,5 +1,6 @@
 // ntbc_api.cu -- host side of libntbc.so: the C ABI declared in include/ntbc.h.
 // Model parsing/validation, device residency, operand re-layout, kernel launches, error reporting.
+#include <cuda.h>  // driver types only (entry points resolved at run time, no -lcuda)
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -127,6 +128,8 @@ int round16(int v) { return (v + 15) & ~15; }
 
 }  // namespace
 
+constexpr int kMaxChunks = 64;
+
 struct ntbc_model_s {
   int device;
   Arch arch;
@@ -138,6 +141,20 @@ struct ntbc_model_s {
   // lazily sized scratch for ntbc_decode_material_host
   uint8_t* d_scratch = nullptr;
   size_t scratch_bytes = 0;
+  // pipelined device->host copies of ntbc_decode_material_host: the fused kernel counts finished
+  // units per row chunk in d_progress (monotonic across calls); a copy stream waits on each counter
+  // (stream memory operation) and copies that chunk while the kernel works on later rows.
+  unsigned long long* d_progress = nullptr;
+  unsigned long long progress_target[kMaxChunks] = {};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_start = nullptr, copy_done = nullptr;
+  // double-buffered weights for ntbc_decode_material_host: the next call uploads into the other slot
+  // on upload_stream while the previous call's kernel still reads the current one.
+  uint8_t* slot_blob[2] = {nullptr, nullptr};
+  uint8_t* slot_img[2] = {nullptr, nullptr};
+  int cur = 0;
+  cudaStream_t upload_stream = nullptr;
+  cudaEvent_t uploaded = nullptr, slot_free[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -166,7 +183,7 @@ void layout_nets(ntbc_model_s* m) {
 
 ntbc_status upload(ntbc_model_s* m, const void* blob, size_t n, cudaStream_t st) {
   const Arch& a = m->arch;
-  CUDA_TRY(cudaMemcpyAsync(m->d_blob, blob, n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(m->d_blob, blob, n, cudaMemcpyHostToDevice, st));  // into the current slot
   for (int k = 0; k < 2; k++)
     for (int l = 0; l < 4; l++) {
       const int kin16 = l == 0 ? 16 : a.hidden, npad = l < 3 ? a.hidden : round16(a.dims[k][4]);
@@ -267,6 +284,67 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
   return fail(NTBC_EINVAL, "unsupported hidden width");
 }
 
+// cuStreamWaitValue64 through the runtime's driver entry-point query (no link-time libcuda dependency)
+typedef CUresult (*wait64_fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*dev_attr_fn)(int*, CUdevice_attribute, CUdevice);
+typedef CUresult (*dev_get_fn)(CUdevice*, int);
+wait64_fn g_wait64 = nullptr;
+
+bool stream_waits_supported(int device) {
+  static int cached[64];  // 0 unknown, 1 yes, 2 no
+  if (device < 0 || device >= 64) return false;
+  if (cached[device]) return cached[device] == 1;
+  if (const char* e = getenv("NTBC_NO_PIPELINED_COPY")) if (atoi(e)) { cached[device] = 2; return false; }
+  void *w = nullptr, *ga = nullptr, *gd = nullptr;
+  cudaDriverEntryPointQueryResult q1, q2, q3;
+  bool ok = cudaGetDriverEntryPoint("cuStreamWaitValue64", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess &&
+            cudaGetDriverEntryPoint("cuDeviceGetAttribute", &ga, cudaEnableDefault, &q2) == cudaSuccess &&
+            q2 == cudaDriverEntryPointSuccess &&
+            cudaGetDriverEntryPoint("cuDeviceGet", &gd, cudaEnableDefault, &q3) == cudaSuccess &&
+            q3 == cudaDriverEntryPointSuccess;
+  if (ok) {
+    CUdevice d;
+    int v = 0;
+    ok = ((dev_get_fn)gd)(&d, device) == CUDA_SUCCESS &&
+         ((dev_attr_fn)ga)(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, d) == CUDA_SUCCESS && v;
+  }
+  cudaGetLastError();
+  if (ok) g_wait64 = (wait64_fn)w;
+  cached[device] = ok ? 1 : 2;
+  return ok;
+}
+
+// streams, events, progress counters and the second weight slot of the pipelined host path
+// (allocated once per model; on failure the host path falls back to serial copies on `stream`)
+bool ensure_copy_state(ntbc_model_s* m) {
+  if (m->d_progress) return true;
+  const unsigned f = cudaEventDisableTiming;
+  bool ok = cudaMalloc(&m->slot_blob[1], m->blob_cap) == cudaSuccess &&
+            cudaMalloc(&m->slot_img[1], m->img_bytes) == cudaSuccess &&
+            cudaMemset(m->slot_img[1], 0, m->img_bytes) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&m->upload_stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&m->copy_start, f) == cudaSuccess &&
+            cudaEventCreateWithFlags(&m->copy_done, f) == cudaSuccess &&
+            cudaEventCreateWithFlags(&m->uploaded, f) == cudaSuccess &&
+            cudaEventCreateWithFlags(&m->slot_free[0], f) == cudaSuccess &&
+            cudaEventCreateWithFlags(&m->slot_free[1], f) == cudaSuccess &&
+            cudaMalloc(&m->d_progress, kMaxChunks * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMemset(m->d_progress, 0, kMaxChunks * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaDeviceSynchronize() == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    cudaFree(m->d_progress);
+    m->d_progress = nullptr;
+    return false;
+  }
+  m->slot_blob[0] = m->d_blob;
+  m->slot_img[0] = m->d_img;
+  m->cur = 0;
+  return true;
+}
+
 ntbc_status check_dims(int W, int H, int r0, int r1) {
   if (W <= 0 || H <= 0 || W % 4 || H % 4) return fail(NTBC_EINVAL, "width/height %dx%d must be positive multiples of 4", W, H);
   if (r0 < 0 || r0 >= r1 || r1 > H / 4) return fail(NTBC_EINVAL, "block rows [%d,%d) not within [0,%d)", r0, r1, H / 4);
@@ -332,16 +410,25 @@ ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out) {
   out->texel_levels = a.levels[1];
   out->texel_coarsest = a.coarsest[1];
   out->features = a.F;
-  out->device_bytes = m->blob_cap + m->img_bytes + m->scratch_bytes;
+  out->device_bytes = (m->blob_cap + m->img_bytes) * (m->slot_blob[1] ? 2 : 1) + m->scratch_bytes;
   return NTBC_OK;
 }
 
 void ntbc_free_model(ntbc_model m) {
   if (!m) return;
   DevGuard dg(m->device);
-  cudaFree(m->d_blob);
-  cudaFree(m->d_img);
+  cudaFree(m->slot_blob[0] ? m->slot_blob[0] : m->d_blob);
+  cudaFree(m->slot_img[0] ? m->slot_img[0] : m->d_img);
   cudaFree(m->d_scratch);
+  cudaFree(m->d_progress);
+  if (m->copy_start) cudaEventDestroy(m->copy_start);
+  if (m->copy_done) cudaEventDestroy(m->copy_done);
+  if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  for (int i = 0; i < 2; i++) if (m->slot_free[i]) cudaEventDestroy(m->slot_free[i]);
+  if (m->uploaded) cudaEventDestroy(m->uploaded);
+  if (m->upload_stream) cudaStreamDestroy(m->upload_stream);
+  cudaFree(m->slot_blob[1]);
+  cudaFree(m->slot_img[1]);
   delete m;
 }
 
@@ -382,14 +469,25 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
   if (n_models < 1 || n_models > 2) return fail(NTBC_EINVAL, "n_models %d not in {1,2}", n_models);
   ntbc_status st = check_dims(width, height, 0, height / 4);
   if (st) return st;
-  const size_t plane = (size_t)(width / 4) * (height / 4) * 8;
-  void* dev_out[2 * kMaxTex];
+  if (n_models == 2) {  // reuse the pair validation of ntbc_decode_material without launching anything
+    for (int i = 0; i < 2; i++) if (!models[i]) return fail(NTBC_EINVAL, "model %d is NULL", i);
+    auto all = [](const Arch& a, int f) { for (int k = 0; k < a.n_tex; k++) if (a.fmt[k] != f) return false; return true; };
+    const Arch &x = models[0]->arch, &y = models[1]->arch;
+    if (!((all(x, NTBC_BC1) && all(y, NTBC_BC4)) || (all(x, NTBC_BC4) && all(y, NTBC_BC1))))
+      return fail(NTBC_EMISMATCH, "conservative pair must be one all-BC1 and one all-BC4 model");
+  }
+  const int BW = width / 4, BH = height / 4;
+  const size_t plane = (size_t)BW * BH * 8, row_bytes = (size_t)BW * 8;
+  cudaStream_t cs = (cudaStream_t)stream;
   int t = 0;
   for (int i = 0; i < n_models; i++) {
     ntbc_model_s* m = models[i];
     if (!m) return fail(NTBC_EINVAL, "model %d is NULL", i);
     DevGuard dg(m->device);
-    const size_t need = plane * m->arch.n_tex;
+    const int n_tex = m->arch.n_tex;
+    for (int k = 0; k < n_tex; k++)
+      if (!host_out[t + k]) return fail(NTBC_EINVAL, "host_out[%d] is NULL", t + k);
+    const size_t need = plane * n_tex;
     if (m->scratch_bytes < need) {
       cudaFree(m->d_scratch);
       m->d_scratch = nullptr;
@@ -397,15 +495,65 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
       if (cudaMalloc(&m->d_scratch, need) != cudaSuccess) { cudaGetLastError(); return fail(NTBC_ENOMEM, "scratch %zu B", need); }
       m->scratch_bytes = need;
     }
-    st = ntbc_model_upload_async(m, blobs[i], blob_sizes[i], stream);
+    FusedParams p{};
+    p.W = width; p.H = height; p.row_begin = 0; p.row_end = BH;
+    for (int k = 0; k < n_tex; k++) p.out[k] = (uint64_t*)(m->d_scratch + k * plane);
+    // row chunks for the pipelined copy-back: ~16 chunks of whole block rows
+    const int upr = (BW + kUnitBlocks - 1) / kUnitBlocks;
+    const int rows_per_chunk = std::max(1, (BH + 15) / 16);  // 16 chunks: best of 4/8/16/32 measured
+    const int n_chunks = (BH + rows_per_chunk - 1) / rows_per_chunk;
+    const bool pipelined = stream_waits_supported(m->device) && n_chunks <= kMaxChunks && ensure_copy_state(m);
+    if (!pipelined) {
+      st = ntbc_model_upload_async(m, blobs[i], blob_sizes[i], stream);
+      if (st) return st;
+    } else {
+      // upload into the idle weight slot on upload_stream (overlaps the previous call's kernel),
+      // once the last kernel that read that slot has finished; the kernel below waits for it.
+      Arch a;
+      st = parse(blobs[i], blob_sizes[i], a);
+      if (st) return st;
+      if (!same_arch(a, m->arch)) return fail(NTBC_EMISMATCH, "blob architecture differs from the loaded model");
+      const int s = m->cur ^ 1;
+      m->arch = a;
+      m->cur = s;
+      m->d_blob = m->slot_blob[s];
+      m->d_img = m->slot_img[s];
+      CUDA_TRY(cudaStreamWaitEvent(m->upload_stream, m->slot_free[s], 0));
+      st = upload(m, blobs[i], blob_sizes[i], m->upload_stream);
+      if (st) return st;
+      CUDA_TRY(cudaEventRecord(m->uploaded, m->upload_stream));
+      CUDA_TRY(cudaStreamWaitEvent(cs, m->uploaded, 0));
+    }
+    if (pipelined) {
+      p.progress = m->d_progress;
+      p.chunk_units = rows_per_chunk * upr;
+    }
+    if (pipelined) {  // copy stream: ordered after the upload and whatever precedes it on `stream`
+      CUDA_TRY(cudaEventRecord(m->copy_start, cs));
+      CUDA_TRY(cudaStreamWaitEvent(m->copy_stream, m->copy_start, 0));
+    }
+    st = launch_fused(m, p, false, cs);
     if (st) return st;
-    for (int k = 0; k < m->arch.n_tex; k++) dev_out[t++] = m->d_scratch + k * plane;
-  }
-  st = ntbc_decode_material(models, n_models, width, height, 0, height / 4, dev_out, stream);
-  if (st) return st;
-  for (int k = 0; k < t; k++) {
-    if (!host_out[k]) return fail(NTBC_EINVAL, "host_out[%d] is NULL", k);
-    CUDA_TRY(cudaMemcpyAsync(host_out[k], dev_out[k], plane, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    if (pipelined) CUDA_TRY(cudaEventRecord(m->slot_free[m->cur], cs));
+    if (!pipelined) {
+      for (int k = 0; k < n_tex; k++)
+        CUDA_TRY(cudaMemcpyAsync(host_out[t + k], p.out[k], plane, cudaMemcpyDeviceToHost, cs));
+    } else {
+      // chunk c's copies wait until all units of chunk c have been published by the running kernel
+      for (int c = 0; c < n_chunks; c++) {
+        const int r0 = c * rows_per_chunk, r1 = std::min(BH, r0 + rows_per_chunk);
+        m->progress_target[c] += (unsigned long long)(r1 - r0) * upr;
+        if (g_wait64((CUstream)m->copy_stream, (CUdeviceptr)(m->d_progress + c), m->progress_target[c],
+                     CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+          return fail(NTBC_ECUDA, "stream wait on progress counter failed");
+        for (int k = 0; k < n_tex; k++)
+          CUDA_TRY(cudaMemcpyAsync((uint8_t*)host_out[t + k] + r0 * row_bytes, (const uint8_t*)p.out[k] + r0 * row_bytes,
+                                   (size_t)(r1 - r0) * row_bytes, cudaMemcpyDeviceToHost, m->copy_stream));
+      }
+      CUDA_TRY(cudaEventRecord(m->copy_done, m->copy_stream));
+      CUDA_TRY(cudaStreamWaitEvent(cs, m->copy_done, 0));  // the caller's stream sees the finished copies
+    }
+    t += n_tex;
   }
   return NTBC_OK;
 }

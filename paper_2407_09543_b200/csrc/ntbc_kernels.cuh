@@ -48,6 +48,8 @@ struct FusedParams {
   uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
   uint32_t debug_flags;         // bit 1: grid-feature dump (ntbc_debug_features)
   int k23;                      // = 1 << 23 (run-time constant, see selu2_h2)
+  unsigned long long* progress; // optional: per-chunk count of finished units (pipelined D2H, see ntbc_api.cu)
+  int chunk_units;              // units per progress chunk
 };
 
 // ---------------------------------------------------------------- a1-a2: coordinates + grid encode
@@ -328,6 +330,13 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           }
           if ((lane & 15) == 0 && b < nvalid) p.out[k][out_row + bx] = word;
         }
+      }
+    }
+    if (!DUMP && p.progress) {  // publish the finished unit: CTA barrier, then one system-scope release
+      named_bar_sync(bar_id, 128);
+      if (r == 0) {
+        __threadfence_system();   // the consumer is the copy engine (measured: same cost as a gpu fence)
+        atomicAdd(p.progress + u / p.chunk_units, 1ull);
       }
     }
   }

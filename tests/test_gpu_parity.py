@@ -211,6 +211,14 @@ def test_conservative_pair_and_mismatch_rules(ntbc):
         assert np.array_equal(u64(outs[k]), ref[k])
     with pytest.raises(ntbc.NtbcError):   # two all-BC1 models are not a conservative pair
         ntbc.decode_material([ms[0], ms[0]], W, H)
+    # the same pair through the pipelined host entry point (two models, two uploads, one call)
+    pinned = [torch.frombuffer(bytearray(b), dtype=torch.uint8).pin_memory() for b in (rgb, sc)]
+    host = [torch.full((H // 4, W // 4), -1, dtype=torch.int64).pin_memory() for _ in range(6)]
+    for _ in range(2):
+        ntbc.decode_material_host(ms, pinned, W, H, host)
+        torch.cuda.synchronize()
+        for k in range(6):
+            assert np.array_equal(host[k].numpy().view(np.uint64), ref[k])
 
 
 def test_row_shards_union_equals_full(ntbc):
@@ -236,6 +244,28 @@ def test_host_entry_point_matches_device_path(ntbc):
     ref = oracle.Model(blob).decode_material(W, H, 0, 4)
     for k in range(m.n_tex):
         assert np.array_equal(host[k].numpy().view(np.uint64)[:4], ref[k])
+
+
+@pytest.mark.parametrize("W,H", [(1024, 1024), (1000, 996), (64, 8)])
+def test_host_entry_point_pipelined_copies(ntbc, W, H):
+    """ntbc_decode_material_host copies row chunks back while the kernel runs (progress counters,
+    DESIGN.md §6): repeated calls with changing weights and ragged shapes must return every word of the
+    device path, and sampled rows (first / last of the texture) must equal the oracle."""
+    m = ntbc.Model(synth.model_blob(2, material=0))
+    for material in (1, 2, 1):
+        blob = synth.model_blob(2, material=material)
+        pinned = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
+        host = [torch.full((H // 4, W // 4), -1, dtype=torch.int64).pin_memory() for _ in range(m.n_tex)]
+        ntbc.decode_material_host([m], [pinned], W, H, host)
+        torch.cuda.synchronize()
+        dev = ntbc.decode_material([m], W, H)
+        for k in range(m.n_tex):
+            assert torch.equal(host[k], dev[k].cpu())
+        om = oracle.Model(blob)
+        for r0, r1 in ((0, 1), (H // 4 - 1, H // 4)):
+            ref = om.decode_material(W, H, r0, r1)
+            for k in range(m.n_tex):
+                assert np.array_equal(host[k].numpy().view(np.uint64)[r0:r1], ref[k])
 
 
 def test_psnr_agreement(ntbc):

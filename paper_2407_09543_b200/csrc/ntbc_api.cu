@@ -203,15 +203,15 @@ struct DevGuard {
   ~DevGuard() { int cur; cudaGetDevice(&cur); if (prev >= 0 && cur != prev) cudaSetDevice(prev); }
 };
 
-template <int H, int NWG, bool DUMP>
+template <int H, int NWG, int SPLIT, bool DUMP>
 ntbc_status launch_fused_t(const FusedParams& p, size_t smem, int grid, cudaStream_t st) {
-  auto kern = fused_decode_kernel<H, NWG, DUMP>;
+  auto kern = fused_decode_kernel<H, NWG, SPLIT, DUMP>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
-  kern<<<grid, NWG * 128, smem, st>>>(p);
+  kern<<<grid, NWG * 128 * SPLIT, smem, st>>>(p);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return NTBC_OK;
@@ -234,6 +234,15 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
       p.lv[g][l].res = a.coarsest[g] << l;
       p.lv[g][l].s = a.s[g][l];
       p.lv[g][l].z = a.z[g][l];
+    }
+    // levels past the grid's count read level 0 with s = 0, z = 0: the lookup then yields exactly +0
+    // (s*d = +-0, every lerp of signed zeros is +0), the zero feature the architecture defines, so
+    // the kernel samples all kMaxLevels levels without branches and can batch their loads.
+    for (int l = a.levels[g]; l < kMaxLevels; l++) {
+      p.lv[g][l].offset = (uint32_t)a.level_off[g][0];
+      p.lv[g][l].res = a.coarsest[g];
+      p.lv[g][l].s = 0.0f;
+      p.lv[g][l].z = 0;
     }
   }
   p.net[0] = m->net[0];
@@ -260,26 +269,44 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t cap = 227 * 1024;
   int nwg = fused_smem(p, 4) <= cap ? 4 : fused_smem(p, 3) <= cap ? 3 : 2;
+  int split = 1;
+  if (const char* e = getenv("NTBC_SPLIT")) split = atoi(e) == 2 ? 2 : 1;   // measurement override
+  if (a.hidden < 32) split = 1;
+  if (split == 2) nwg = std::min(nwg, 3);
   if (const char* e = getenv("NTBC_NWG")) {  // measurement override (bench sweeps); clamped to what fits
     const int want = atoi(e);
-    if (want >= 2 && want <= 4 && fused_smem(p, want) <= cap) nwg = want;
+    if (want >= 2 && want <= (split == 2 ? 3 : 4) && fused_smem(p, want) <= cap) nwg = want;
+  }
+  // output channels of the textures each half of a SPLIT work group owns (texture k -> half k % 2)
+  for (int n = 0; n < 2; n++) {
+    p.chan_mask[n][0] = p.chan_mask[n][1] = 0;
+    for (int k = 0; k < a.n_tex; k++) {
+      const int off = n == 0 ? p.ep_off[k] : p.col_off[k];
+      const int w = n == 0 ? (a.fmt[k] == NTBC_BC1 ? 6 : 2) : (a.fmt[k] == NTBC_BC1 ? 3 : 1);
+      for (int c = off; c < off + w; c++) p.chan_mask[n][split == 2 ? (k & 1) : 0] |= 1ull << c;
+    }
   }
   const size_t smem = fused_smem(p, nwg);
   if (smem > cap) return fail(NTBC_EINVAL, "model needs %zu B of shared memory (> %zu)", smem, cap);
   int grid = (p.n_units + nwg - 1) / nwg;
   if (grid > sms) grid = sms;
   if (grid < 1) grid = 1;
-#define NTBC_DISPATCH(HH)                                                                        \
-  if (a.hidden == HH) {                                                                          \
-    if (nwg == 4) return dump ? launch_fused_t<HH, 4, true>(p, smem, grid, st)                   \
-                              : launch_fused_t<HH, 4, false>(p, smem, grid, st);                 \
-    if (nwg == 3) return dump ? launch_fused_t<HH, 3, true>(p, smem, grid, st)                   \
-                              : launch_fused_t<HH, 3, false>(p, smem, grid, st);                 \
-    return dump ? launch_fused_t<HH, 2, true>(p, smem, grid, st) : launch_fused_t<HH, 2, false>(p, smem, grid, st); \
+#define NTBC_LAUNCH(HH, NW, SP) \
+  return dump ? launch_fused_t<HH, NW, SP, true>(p, smem, grid, st) : launch_fused_t<HH, NW, SP, false>(p, smem, grid, st);
+#define NTBC_DISPATCH(HH)                                     \
+  if (a.hidden == HH) {                                       \
+    if (split == 2 && HH >= 32) {                             \
+      if (nwg == 3) { NTBC_LAUNCH(HH, 3, (HH >= 32 ? 2 : 1)) } \
+      NTBC_LAUNCH(HH, 2, (HH >= 32 ? 2 : 1))                  \
+    }                                                         \
+    if (nwg == 4) { NTBC_LAUNCH(HH, 4, 1) }                   \
+    if (nwg == 3) { NTBC_LAUNCH(HH, 3, 1) }                   \
+    NTBC_LAUNCH(HH, 2, 1)                                     \
   }
   NTBC_DISPATCH(16)
   NTBC_DISPATCH(32)
   NTBC_DISPATCH(64)
+#undef NTBC_LAUNCH
 #undef NTBC_DISPATCH
   return fail(NTBC_EINVAL, "unsupported hidden width");
 }

@@ -48,6 +48,7 @@ struct FusedParams {
   uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
   uint32_t debug_flags;         // bit 1: grid-feature dump (ntbc_debug_features)
   int k23;                      // = 1 << 23 (run-time constant, see selu2_h2)
+  uint64_t chan_mask[2][2];     // [net][half]: output channels whose sigmoid this half computes (SPLIT)
   unsigned long long* progress; // optional: per-chunk count of finished units (pipelined D2H, see ntbc_api.cu)
   int chunk_units;              // units per progress chunk
 };
@@ -89,23 +90,6 @@ __device__ __forceinline__ uint64_t level_lookup2(const uint8_t* blob, const Gri
   return fma2(FY, sub2(bot, top), top);
 }
 
-// 16 features (levels coarse->fine, 2 per level, R3) of grid g at (pu, pv), rounded to fp16 and
-// written as row `row` of a K-major [128][K] operand (columns 0..15; unused levels are zero).
-__device__ __forceinline__ void write_feature_row(const FusedParams& p, int g, float pu, float pv, uint8_t* A,
-                                                  int row, int K, float* dump = nullptr) {
-  uint32_t h[8];
-#pragma unroll
-  for (int l = 0; l < kMaxLevels; l++) {
-    float f0 = 0.0f, f1 = 0.0f;
-    if (l < p.levels[g]) f2unpack(level_lookup2(p.blob, p.lv[g][l], pu, pv), f0, f1);
-    if (dump) { dump[2 * l] = f0; dump[2 * l + 1] = f1; }
-    const __half2 v = __floats2half2_rn(f0, f1);
-    h[l] = *reinterpret_cast<const uint32_t*>(&v);
-  }
-  *reinterpret_cast<uint4*>(A + kmajor_offset(row, 0, K)) = make_uint4(h[0], h[1], h[2], h[3]);
-  *reinterpret_cast<uint4*>(A + kmajor_offset(row, 8, K)) = make_uint4(h[4], h[5], h[6], h[7]);
-}
-
 // ---------------------------------------------------------------- TMEM load helper (x16 columns)
 __device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* r) {
   asm volatile(
@@ -144,13 +128,22 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, in
 }
 
 // ---------------------------------------------------------------- kernel (1): fused decode
-// One CTA per SM, NWG independent 128-thread work groups; each work group owns 64 TMEM columns,
-// an A-operand buffer and a palette buffer, and loops over work units of 128 block positions of
-// one block row: one endpoint tile (128 blocks) then up to 16 colour tiles (8 blocks = 128 texels).
-template <int H, int NWG, bool DUMP>
-__global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
+// One CTA per SM, NWG independent work groups of SPLIT x 4 warps.  A work group owns 64 TMEM columns,
+// an A-operand buffer and a palette buffer, and loops over work units of 128 block positions of one
+// block row: one endpoint tile (128 blocks) then up to 16 colour tiles (8 blocks = 128 texels).
+// Row r of a tile lives in TMEM lane r, so it is handled by the warps with (warp % 4) == r / 32; with
+// SPLIT = 2 two warps share each lane quarter and split the work of a row: grid levels 0-3 / 4-7,
+// hidden columns [0, H/2) / [H/2, H), textures k % 2 == 0 / 1.  More warps per SM hide the latency of
+// the dependent epilogue chains at the same register file.
+template <int H, int NWG, int SPLIT, bool DUMP>
+__global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
+  constexpr int GT = 128 * SPLIT;   // threads per work group
+  constexpr int HC = H / SPLIT;     // hidden columns per thread
+  static_assert(HC % 16 == 0, "hidden columns per thread must be a multiple of 16");
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, wg = tid / GT, gt = tid % GT, warp = tid >> 5, lane = tid & 31;
+  const int r = gt & 127, half = gt >> 7;   // tile row (= TMEM lane) and share of the row's work
+  const bool leader = gt == 0;
 
   // ---- carve shared memory
   uint8_t* img_e = smem;                                          // endpoint net operand image
@@ -197,6 +190,27 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   const uint32_t img_base[2] = {smem_u32(img_e), smem_u32(img_c)};
   const int bar_id = 1 + wg;
   uint32_t phase = 0;
+  // textures (and hence output channels) handled by this thread
+  auto mine = [&](int k) { return SPLIT == 1 || (k % SPLIT) == half; };
+
+  // 16 grid features of row r (levels coarse->fine, 2 per level, R3) -> fp16 -> A columns 0..15;
+  // with SPLIT = 2 this thread does levels [8/SPLIT * half, ...) (one 16-B store)
+  auto features = [&](int g, float pu, float pv, float* dump) {
+    constexpr int LPT = kMaxLevels / SPLIT;
+    uint32_t hv[LPT];
+#pragma unroll
+    for (int i = 0; i < LPT; i++) {
+      const int l = LPT * half + i;
+      float f0, f1;   // all levels unconditionally: unused ones are set up to return +0 (launch_fused)
+      f2unpack(level_lookup2(p.blob, p.lv[g][l], pu, pv), f0, f1);
+      if (dump) { dump[2 * l] = f0; dump[2 * l + 1] = f1; }
+      const __half2 v = __floats2half2_rn(f0, f1);
+      hv[i] = *reinterpret_cast<const uint32_t*>(&v);
+    }
+#pragma unroll
+    for (int i = 0; i < LPT; i += 4)
+      *reinterpret_cast<uint4*>(A + kmajor_offset(r, 2 * (LPT * half + i), H)) = make_uint4(hv[i], hv[i + 1], hv[i + 2], hv[i + 3]);
+  };
 
   // run the 4-layer MLP of net `n` on the A rows already written; leaves the output layer in TMEM
   auto run_mlp = [&](int n) {
@@ -204,45 +218,57 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     for (int l = 0; l < 4; l++) {
       fence_async_smem();
       tc_fence_before();
-      named_bar_sync(bar_id, 128);
-      if (r == 0) {
+      named_bar_sync(bar_id, GT);
+      if (leader) {
         tc_fence_after();
         const int kin16 = l == 0 ? 16 : H;
         const int N = l < 3 ? H : p.net[n].n_out16;
         issue_layer(tm, a_base, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
         mma_commit(bar_mma);
       }
-      if (r == 0) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
-      named_bar_sync(bar_id, 128);
+      if (leader) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
+      named_bar_sync(bar_id, GT);
       phase ^= 1u;
       tc_fence_after();
       if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10), 16 columns at a time
+        const uint32_t t0 = tm_row + half * HC;
         uint32_t buf[2][16];
-        tmem_ld16p(tm_row, buf[0]);
+        tmem_ld16p(t0, buf[0]);
         tmem_wait_ld16(buf[0]);
 #pragma unroll
-        for (int c = 0; c < H / 16; c++) {
-          if (c + 1 < H / 16) tmem_ld16p(tm_row + (c + 1) * 16, buf[(c + 1) & 1]);   // prefetch next chunk
+        for (int c = 0; c < HC / 16; c++) {
+          if (c + 1 < HC / 16) tmem_ld16p(t0 + (c + 1) * 16, buf[(c + 1) & 1]);   // prefetch next chunk
           uint32_t hv[8];
 #pragma unroll
           for (int j = 0; j < 8; j++)
             hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]), p.k23);
-          *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-          *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
-          if (c + 1 < H / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
+          const int col = half * HC + c * 16;
+          *reinterpret_cast<uint4*>(A + kmajor_offset(r, col, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+          *reinterpret_cast<uint4*>(A + kmajor_offset(r, col + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+          if (c + 1 < HC / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
         }
       }
     }
   };
-  // output layer epilogue: sigmoid of the n_out columns (pairs, rounded up) -> fp32 staging [ch][128]
+  // output layer epilogue: sigmoid of this thread's output channels (pairs) -> fp32 staging [ch][128]
   auto stage_outputs = [&](int n) {
+    const uint64_t own = DUMP ? ~0ull : p.chan_mask[n][SPLIT == 1 ? 0 : half];
     const int no = p.net[n].n_out;
 #pragma unroll 1
-    for (int ch = 0; ch < no; ch += 2) {
-      uint32_t a, b;
-      tmem_ld2(tm_row + ch, a, b);
-      stage[ch * 128 + r] = sigmoid(__uint_as_float(a));
-      stage[(ch + 1) * 128 + r] = sigmoid(__uint_as_float(b));
+    for (int c16 = 0; c16 < no; c16 += 16) {
+      uint32_t v[16];
+      tmem_ld16p(tm_row + c16, v);
+      tmem_wait_ld16(v);
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const int ch = c16 + j;
+        if (ch < no && ((own >> ch) & 3ull)) {
+          float s0, s1;
+          sigmoid2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), s0, s1);
+          stage[ch * 128 + r] = s0;
+          stage[(ch + 1) * 128 + r] = s1;
+        }
+      }
     }
   };
 
@@ -254,21 +280,22 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     const size_t out_row = (size_t)(by - p.row_begin) * p.BW;
 
     // ================= endpoint tile: row r = block (bx0 + r, by)  (rows a1-a3, a5-a6)
-    named_bar_sync(bar_id, 128);  // previous tile's readers of A / staging / palettes are done
+    named_bar_sync(bar_id, GT);  // previous tile's readers of A / staging / palettes are done
     {
       const float s = __fdiv_rn(__fadd_rn((float)min(bx0 + r, p.BW - 1), 0.5f), (float)p.BW);
       const float t = __fdiv_rn(__fadd_rn((float)by, 0.5f), (float)p.BH);
       float* fd = (DUMP && (p.debug_flags & 2) && r < nvalid) ? p.dump_ep + (out_row + bx0 + r) * 16 : nullptr;
-      write_feature_row(p, 0, s, t, A, r, H, fd);
+      features(0, s, t, fd);
     }
     run_mlp(0);
     stage_outputs(0);
     if (DUMP) {
-      if (r < nvalid && !(p.debug_flags & 2))
+      if (half == 0 && r < nvalid && !(p.debug_flags & 2))
         for (int ch = 0; ch < p.net[0].n_out; ch++)
           p.dump_ep[(out_row + bx0 + r) * p.net[0].n_out + ch] = stage[ch * 128 + r];
     } else {
       for (int k = 0; k < p.n_tex; k++) {
+        if (!mine(k)) continue;
         const int eo = p.ep_off[k];
         float4* slot = reinterpret_cast<float4*>(pal + ((size_t)k * 128 + r) * 8);
         if (p.fmt[k] == kFmtBC1) {  // slot = quantized endpoints e0q, e1q (R11, R12)
@@ -296,22 +323,23 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     for (int j = 0; j < kUnitBlocks / 8 && 8 * j < nvalid; j++) {
       const int b = 8 * j + (r >> 4), i = r & 15;
       const int bx = bx0 + b, x = 4 * min(bx, p.BW - 1) + (i & 3), y = 4 * by + (i >> 2);
-      named_bar_sync(bar_id, 128);
+      named_bar_sync(bar_id, GT);
       {
         const float pu = __fdiv_rn(__fadd_rn((float)x, 0.5f), (float)p.W);
         const float pv = __fdiv_rn(__fadd_rn((float)y, 0.5f), (float)p.H);
         float* fd = (DUMP && (p.debug_flags & 2) && b < nvalid)
                         ? p.dump_col + (((size_t)(y - 4 * p.row_begin)) * p.W + x) * 16 : nullptr;
-        write_feature_row(p, 1, pu, pv, A, r, H, fd);
+        features(1, pu, pv, fd);
       }
       run_mlp(1);
       stage_outputs(1);
       if (DUMP) {
-        if (b < nvalid && !(p.debug_flags & 2))
+        if (half == 0 && b < nvalid && !(p.debug_flags & 2))
           for (int ch = 0; ch < p.net[1].n_out; ch++)
             p.dump_col[(((size_t)(y - 4 * p.row_begin)) * p.W + x) * p.net[1].n_out + ch] = stage[ch * 128 + r];
       } else {
         for (int k = 0; k < p.n_tex; k++) {
+          if (!mine(k)) continue;
           const int co = p.col_off[k];
           const float4* slot = reinterpret_cast<const float4*>(pal + ((size_t)k * 128 + b) * 8);
           const uint32_t hdr = hdrs[k * 128 + b];
@@ -332,9 +360,9 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
         }
       }
     }
-    if (!DUMP && p.progress) {  // publish the finished unit: CTA barrier, then one system-scope release
-      named_bar_sync(bar_id, 128);
-      if (r == 0) {
+    if (!DUMP && p.progress) {  // publish the finished unit: group barrier, then one system-scope release
+      named_bar_sync(bar_id, GT);
+      if (leader) {
         __threadfence_system();   // the consumer is the copy engine (measured: same cost as a gpu fence)
         atomicAdd(p.progress + u / p.chunk_units, 1ull);
       }

@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libntbc.so")
+# NTBC_LIB selects another in-tree build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.path.join(_HERE, os.environ.get("NTBC_LIB", "libntbc.so"))
 BC1, BC4 = 1, 4
 
 if not os.path.exists(LIB_PATH):

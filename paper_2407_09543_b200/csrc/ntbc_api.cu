@@ -218,8 +218,8 @@ ntbc_status launch_fused_t(const FusedParams& p, size_t smem, int grid, cudaStre
 }
 
 size_t fused_smem(const FusedParams& p, int nwg) {
-  return (size_t)p.net[0].img_bytes + p.net[1].img_bytes + 4096 + (size_t)nwg * (p.a_bytes + p.pal_bytes) +
-         8 * (1 + nwg) + 16;
+  return (size_t)p.net[0].img_bytes + p.net[1].img_bytes + 4096 + kUnormBytes +
+         (size_t)nwg * (p.a_bytes + p.pal_bytes) + 8 * (1 + nwg) + 16;
 }
 
 ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
@@ -263,19 +263,24 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
   const int maxo = a.dims[0][4] > a.dims[1][4] ? a.dims[0][4] : a.dims[1][4];
   const uint32_t a_kmajor = 128u * a.hidden * 2u, a_stage = 128u * 4u * (uint32_t)((maxo + 1) & ~1);  // pairs
   p.a_bytes = (uint32_t)((std::max(a_kmajor, a_stage) + 127) & ~127u);
-  p.pal_bytes = (uint32_t)(a.n_tex * 128 * (32 + 4));
+  p.pal_bytes = (uint32_t)(a.n_tex * 128 * 4);   // BC word headers only (palettes rebuilt per texel)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t cap = 227 * 1024;
-  int nwg = fused_smem(p, 4) <= cap ? 4 : fused_smem(p, 3) <= cap ? 3 : 2;
+  // work groups per CTA: more independent groups hide more latency (C3: NWG 4 -> 2.70 ms, 6 -> 2.65 with
+  // 8% wave-quantisation loss, 8 -> 2.46); 5 and 6 quantise badly on power-of-two unit counts
+  // (measured for H = 64 only; the H = 32 model of C2 runs 0.19 ms at NWG 4 and 0.34 ms at 8)
+  int nwg = 2;
+  for (int w : {8, 4, 3})
+    if ((w != 8 || a.hidden >= 64) && fused_smem(p, w) <= cap) { nwg = w; break; }
   int split = 1;
   if (const char* e = getenv("NTBC_SPLIT")) split = atoi(e) == 2 ? 2 : 1;   // measurement override
   if (a.hidden < 32) split = 1;
   if (split == 2) nwg = std::min(nwg, 3);
   if (const char* e = getenv("NTBC_NWG")) {  // measurement override (bench sweeps); clamped to what fits
     const int want = atoi(e);
-    if (want >= 2 && want <= (split == 2 ? 3 : 4) && fused_smem(p, want) <= cap) nwg = want;
+    if ((want >= 2 && want <= 6 || want == 8) && (split == 1 || want <= 3) && fused_smem(p, want) <= cap) nwg = want;
   }
   // output channels of the textures each half of a SPLIT work group owns (texture k -> half k % 2)
   for (int n = 0; n < 2; n++) {
@@ -299,6 +304,9 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
       if (nwg == 3) { NTBC_LAUNCH(HH, 3, (HH >= 32 ? 2 : 1)) } \
       NTBC_LAUNCH(HH, 2, (HH >= 32 ? 2 : 1))                  \
     }                                                         \
+    if (nwg == 8) { NTBC_LAUNCH(HH, 8, 1) }                   \
+    if (nwg == 6) { NTBC_LAUNCH(HH, 6, 1) }                   \
+    if (nwg == 5) { NTBC_LAUNCH(HH, 5, 1) }                   \
     if (nwg == 4) { NTBC_LAUNCH(HH, 4, 1) }                   \
     if (nwg == 3) { NTBC_LAUNCH(HH, 3, 1) }                   \
     NTBC_LAUNCH(HH, 2, 1)                                     \

@@ -18,6 +18,10 @@ constexpr int kMaxTex = 8;
 constexpr int kMaxLevels = 8;
 constexpr int kUnitBlocks = 128;  // block positions per work unit = rows of one endpoint MMA tile
 constexpr int kFmtBC1 = 1;
+#ifndef NTBC_PREFETCH_MAXNWG
+#define NTBC_PREFETCH_MAXNWG 4
+#endif
+constexpr int kUnormBytes = 1536;  // 352 fp32 UNORM expansion values (q/31, q/63, q/255) + 32 BC4 weights
 
 struct GridLevel {
   uint32_t offset;  // byte offset of the level payload [res][res][2] in the model blob (device copy)
@@ -149,12 +153,12 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
   uint8_t* img_e = smem;                                          // endpoint net operand image
   uint8_t* img_c = smem + p.net[0].img_bytes;                     // colour net operand image
   uint8_t* ones = img_c + p.net[1].img_bytes;                     // [128][16] K-major, column 0 = 1.0
-  uint8_t* wg_base = ones + 4096 + wg * (p.a_bytes + p.pal_bytes);
+  float* unorm = reinterpret_cast<float*>(ones + 4096);            // q/31 [32], q/63 [64], q/255 [256]
+  uint8_t* wg_base = ones + 4096 + kUnormBytes + wg * (p.a_bytes + p.pal_bytes);
   uint8_t* A = wg_base;                                           // [128][H] K-major fp16 / fp32 staging
   float* stage = reinterpret_cast<float*>(A);                     // [ch][128] fp32 (after the last MMA)
-  float* pal = reinterpret_cast<float*>(wg_base + p.a_bytes);     // [tex][128 blocks][8] fp32
-  uint32_t* hdrs = reinterpret_cast<uint32_t*>(pal + p.n_tex * 128 * 8);  // [tex][128 blocks] BC word low bits
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ones + 4096 + NWG * (p.a_bytes + p.pal_bytes));
+  uint32_t* hdrs = reinterpret_cast<uint32_t*>(wg_base + p.a_bytes);  // [tex][128 blocks] BC word low bits
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ones + 4096 + kUnormBytes + NWG * (p.a_bytes + p.pal_bytes));
   uint64_t* bar_w = bars;                                         // weights landed
   uint64_t* bar_mma = bars + 1 + wg;                              // this work group's MMA completion
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + NWG);
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
     for (int g = 0; g < NWG; g++) mbar_init(bars + 1 + g, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(tmem_slot, NWG <= 2 ? 128 : 256);
+  if (warp == 0) tmem_alloc(tmem_slot, NWG <= 2 ? 128 : NWG <= 4 ? 256 : 512);
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -180,6 +184,10 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
     *reinterpret_cast<uint4*>(ones + kmajor_offset(tid, 0, 16)) = c0;
     *reinterpret_cast<uint4*>(ones + kmajor_offset(tid, 8, 16)) = z;
   }
+  for (int i = tid; i < 352; i += NWG * 128)  // UNORM expansion tables: the exact quotients of R12/R13
+    unorm[i] = i < 32 ? __fdiv_rn((float)i, 31.0f) : i < 96 ? __fdiv_rn((float)(i - 32), 63.0f)
+                                                             : __fdiv_rn((float)(i - 96), 255.0f);
+  if (tid < 32) unorm[352 + tid] = bc4_weight(tid);   // BC4 interpolation weights per mode
   fence_async_smem();
   mbar_wait(bar_w, 0);
   __syncthreads();
@@ -232,12 +240,17 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
       tc_fence_after();
       if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10), 16 columns at a time
         const uint32_t t0 = tm_row + half * HC;
+        constexpr bool PF = NWG <= NTBC_PREFETCH_MAXNWG;   // prefetch the next chunk (needs 16 more registers)
         uint32_t buf[2][16];
         tmem_ld16p(t0, buf[0]);
         tmem_wait_ld16(buf[0]);
 #pragma unroll
         for (int c = 0; c < HC / 16; c++) {
-          if (c + 1 < HC / 16) tmem_ld16p(t0 + (c + 1) * 16, buf[(c + 1) & 1]);   // prefetch next chunk
+          if (!PF && c > 0) {
+            tmem_ld16p(t0 + c * 16, buf[c & 1]);
+            tmem_wait_ld16(buf[c & 1]);
+          }
+          if (PF && c + 1 < HC / 16) tmem_ld16p(t0 + (c + 1) * 16, buf[(c + 1) & 1]);   // prefetch next chunk
           uint32_t hv[8];
 #pragma unroll
           for (int j = 0; j < 8; j++)
@@ -245,7 +258,7 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
           const int col = half * HC + c * 16;
           *reinterpret_cast<uint4*>(A + kmajor_offset(r, col, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
           *reinterpret_cast<uint4*>(A + kmajor_offset(r, col + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
-          if (c + 1 < HC / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
+          if (PF && c + 1 < HC / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
         }
       }
     }
@@ -297,23 +310,14 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
       for (int k = 0; k < p.n_tex; k++) {
         if (!mine(k)) continue;
         const int eo = p.ep_off[k];
-        float4* slot = reinterpret_cast<float4*>(pal + ((size_t)k * 128 + r) * 8);
-        if (p.fmt[k] == kFmtBC1) {  // slot = quantized endpoints e0q, e1q (R11, R12)
-          float ep[6], e0[3], e1[3];
+        if (p.fmt[k] == kFmtBC1) {  // BC word header after quantization and the 4-colour-mode swap (R11, R12)
+          float ep[6];
 #pragma unroll
           for (int c = 0; c < 6; c++) ep[c] = stage[(eo + c) * 128 + r];
-          hdrs[k * 128 + r] = quant_bc1(ep, e0, e1);
-          slot[0] = make_float4(e0[0], e0[1], e0[2], e1[0]);
-          slot[1] = make_float4(e1[1], e1[2], 0.0f, 0.0f);
-        } else {                    // slot = the full 8-entry linear palette (Eq.7/8, R13, R18)
-          float ep[2], e0, e1, pl[8];
-          ep[0] = stage[eo * 128 + r];
-          ep[1] = stage[(eo + 1) * 128 + r];
-          const uint32_t hdr = quant_bc4(ep, e0, e1);
-          hdrs[k * 128 + r] = hdr;
-          bc4_palette(hdr, pl);
-          slot[0] = make_float4(pl[0], pl[1], pl[2], pl[3]);
-          slot[1] = make_float4(pl[4], pl[5], pl[6], pl[7]);
+          hdrs[k * 128 + r] = quant_bc1_hdr(ep);
+        } else {                    // E0 | E1 << 8 (R13)
+          const float ep[2] = {stage[eo * 128 + r], stage[(eo + 1) * 128 + r]};
+          hdrs[k * 128 + r] = quant_bc4_hdr(ep);
         }
       }
     }
@@ -341,19 +345,20 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
         for (int k = 0; k < p.n_tex; k++) {
           if (!mine(k)) continue;
           const int co = p.col_off[k];
-          const float4* slot = reinterpret_cast<const float4*>(pal + ((size_t)k * 128 + b) * 8);
           const uint32_t hdr = hdrs[k * 128 + b];
           uint64_t word;
-          if (p.fmt[k] == kFmtBC1) {
-            const float4 s0 = slot[0], s1 = slot[1];
-            const float e0[3] = {s0.x, s0.y, s0.z}, e1[3] = {s0.w, s1.x, s1.y};
+          if (p.fmt[k] == kFmtBC1) {  // palette endpoints = UNORM expansion of the header (R12)
+            const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
+            const float e0[3] = {unorm[c0 >> 11], unorm[32 + ((c0 >> 5) & 63)], unorm[c0 & 31]};
+            const float e1[3] = {unorm[c1 >> 11], unorm[32 + ((c1 >> 5) & 63)], unorm[c1 & 31]};
             const float c[3] = {stage[co * 128 + r], stage[(co + 1) * 128 + r], stage[(co + 2) * 128 + r]};
-            const uint32_t code = bc1_code(c, e0, e1, (hdr & 0xFFFFu) == (hdr >> 16));
+            const uint32_t code = bc1_code(c, e0, e1, c0 == c1);
             word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
           } else {
-            const float4 s0 = slot[0], s1 = slot[1];
-            const float pl[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-            const uint32_t code = bc4_code(stage[co * 128 + r], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu));
+            const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
+            float pl[8];
+            bc4_palette_tab(unorm[96 + E0], unorm[96 + E1], E0 > E1, unorm + 352, pl);
+            const uint32_t code = bc4_code(stage[co * 128 + r], pl, E0 > E1);
             word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
           }
           if ((lane & 15) == 0 && b < nvalid) p.out[k][out_row + bx] = word;
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
   }
 
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem_base, NWG <= 2 ? 128 : 256);
+  if (warp == 0) tmem_dealloc(tmem_base, NWG <= 2 ? 128 : NWG <= 4 ? 256 : 512);
 }
 
 // ---------------------------------------------------------------- kernel (2): standalone pack (a5-a8)

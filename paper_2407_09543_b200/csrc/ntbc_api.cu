@@ -129,15 +129,21 @@ int round16(int v) { return (v + 15) & ~15; }
 }  // namespace
 
 constexpr int kMaxChunks = 64;
+constexpr int kSchedRing = 64;
+// chunk c is copied on copy stream c % kCopyStreams: each stream-wait operation has a fixed latency,
+// so consecutive chunks' waits must not queue behind each other on one stream
+constexpr int kCopyStreams = 4;
 
 struct ntbc_model_s {
   int device;
   Arch arch;
   uint8_t* d_blob = nullptr;   // device copy of the whole blob (grid payloads read in place)
   size_t blob_cap = 0;
-  uint8_t* d_img = nullptr;    // tcgen05 operand images of both nets
+  // dynamic-scheduling unit counters: a ring of kSchedRing ints, one per launch (zeroed on the
+  // launch's stream), so up to kSchedRing launches of this model may be in flight concurrently
+  int* d_sched = nullptr;
+  std::atomic<unsigned> sched_next{0};
   NetLayout net[2];
-  size_t img_bytes = 0;
   // lazily sized scratch for ntbc_decode_material_host
   uint8_t* d_scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -146,12 +152,11 @@ struct ntbc_model_s {
   // (stream memory operation) and copies that chunk while the kernel works on later rows.
   unsigned long long* d_progress = nullptr;
   unsigned long long progress_target[kMaxChunks] = {};
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t copy_start = nullptr, copy_done = nullptr;
+  cudaStream_t copy_stream[kCopyStreams] = {};
+  cudaEvent_t copy_start = nullptr, copy_done[kCopyStreams] = {};
   // double-buffered weights for ntbc_decode_material_host: the next call uploads into the other slot
   // on upload_stream while the previous call's kernel still reads the current one.
   uint8_t* slot_blob[2] = {nullptr, nullptr};
-  uint8_t* slot_img[2] = {nullptr, nullptr};
   int cur = 0;
   cudaStream_t upload_stream = nullptr;
   cudaEvent_t uploaded = nullptr, slot_free[2] = {nullptr, nullptr};
@@ -159,41 +164,32 @@ struct ntbc_model_s {
 
 namespace {
 
-// B-operand image layout of both nets (K-major, bias folded as an extra K chunk)
+// Shared-memory B-operand images of both nets (K-major, bias folded as an extra K chunk), built by
+// the fused kernel's prologue from the blob's row-major weights (layer offsets and widths here).
 void layout_nets(ntbc_model_s* m) {
   const Arch& a = m->arch;
-  uint32_t off = 0;
   for (int k = 0; k < 2; k++) {
     NetLayout& L = m->net[k];
-    L.img_off = off;
     uint32_t o = 0;
     for (int l = 0; l < 4; l++) {
       const int kin16 = l == 0 ? 16 : a.hidden;
       const int npad = l < 3 ? a.hidden : round16(a.dims[k][4]);
       L.layer_off[l] = o;
+      L.w_off[l] = (uint32_t)a.w_off[k][l];
+      L.b_off[l] = (uint32_t)a.b_off[k][l];
+      L.kin[l] = a.dims[k][l];
+      L.nout[l] = a.dims[k][l + 1];
       o += (uint32_t)(npad * (kin16 + 16) * 2);
     }
     L.img_bytes = o;
     L.n_out = a.dims[k][4];
     L.n_out16 = round16(a.dims[k][4]);
-    off += o;
   }
-  m->img_bytes = off;
 }
 
+// the whole model is the blob: one host->device copy into the current weight slot
 ntbc_status upload(ntbc_model_s* m, const void* blob, size_t n, cudaStream_t st) {
-  const Arch& a = m->arch;
-  CUDA_TRY(cudaMemcpyAsync(m->d_blob, blob, n, cudaMemcpyHostToDevice, st));  // into the current slot
-  for (int k = 0; k < 2; k++)
-    for (int l = 0; l < 4; l++) {
-      const int kin16 = l == 0 ? 16 : a.hidden, npad = l < 3 ? a.hidden : round16(a.dims[k][4]);
-      const int total = npad * (kin16 + 16);
-      relayout_kernel<<<(total + 255) / 256, 256, 0, st>>>(
-          reinterpret_cast<const __half*>(m->d_blob + a.w_off[k][l]), reinterpret_cast<const __half*>(m->d_blob + a.b_off[k][l]),
-          a.dims[k][l], a.dims[k][l + 1], kin16, npad, m->d_img + m->net[k].img_off + m->net[k].layer_off[l]);
-      g_launches++;
-    }
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(m->d_blob, blob, n, cudaMemcpyHostToDevice, st));
   return NTBC_OK;
 }
 
@@ -203,15 +199,15 @@ struct DevGuard {
   ~DevGuard() { int cur; cudaGetDevice(&cur); if (prev >= 0 && cur != prev) cudaSetDevice(prev); }
 };
 
-template <int H, int NWG, int SPLIT, bool DUMP>
+template <int H, int NWG, bool DUMP>
 ntbc_status launch_fused_t(const FusedParams& p, size_t smem, int grid, cudaStream_t st) {
-  auto kern = fused_decode_kernel<H, NWG, SPLIT, DUMP>;
+  auto kern = fused_decode_kernel<H, NWG, DUMP>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
-  kern<<<grid, NWG * 128 * SPLIT, smem, st>>>(p);
+  kern<<<grid, NWG * 128, smem, st>>>(p);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return NTBC_OK;
@@ -219,14 +215,17 @@ ntbc_status launch_fused_t(const FusedParams& p, size_t smem, int grid, cudaStre
 
 size_t fused_smem(const FusedParams& p, int nwg) {
   return (size_t)p.net[0].img_bytes + p.net[1].img_bytes + 4096 + kUnormBytes +
-         (size_t)nwg * (p.a_bytes + p.pal_bytes) + 8 * (1 + nwg) + 16;
+         (size_t)nwg * (p.a_bytes + p.pal_bytes) + 8 * nwg + 16 + 4 * 8;
 }
 
-ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
+ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
   const Arch& a = m->arch;
+  if (!dump && m->d_sched && !(getenv("NTBC_STATIC_SCHED") && atoi(getenv("NTBC_STATIC_SCHED")))) {
+    p.next_unit = m->d_sched + (m->sched_next++ % kSchedRing);
+    CUDA_TRY(cudaMemsetAsync(p.next_unit, 0, sizeof(int), st));
+  }
   p.blob = m->d_blob;
   p.k23 = 1 << 23;
-  p.img = m->d_img;
   for (int g = 0; g < 2; g++) {
     p.levels[g] = a.levels[g];
     for (int l = 0; l < a.levels[g]; l++) {
@@ -274,47 +273,28 @@ ntbc_status launch_fused(const ntbc_model_s* m, FusedParams& p, bool dump, cudaS
   int nwg = 2;
   for (int w : {8, 4, 3})
     if ((w != 8 || a.hidden >= 64) && fused_smem(p, w) <= cap) { nwg = w; break; }
-  int split = 1;
-  if (const char* e = getenv("NTBC_SPLIT")) split = atoi(e) == 2 ? 2 : 1;   // measurement override
-  if (a.hidden < 32) split = 1;
-  if (split == 2) nwg = std::min(nwg, 3);
   if (const char* e = getenv("NTBC_NWG")) {  // measurement override (bench sweeps); clamped to what fits
     const int want = atoi(e);
-    if ((want >= 2 && want <= 6 || want == 8) && (split == 1 || want <= 3) && fused_smem(p, want) <= cap) nwg = want;
-  }
-  // output channels of the textures each half of a SPLIT work group owns (texture k -> half k % 2)
-  for (int n = 0; n < 2; n++) {
-    p.chan_mask[n][0] = p.chan_mask[n][1] = 0;
-    for (int k = 0; k < a.n_tex; k++) {
-      const int off = n == 0 ? p.ep_off[k] : p.col_off[k];
-      const int w = n == 0 ? (a.fmt[k] == NTBC_BC1 ? 6 : 2) : (a.fmt[k] == NTBC_BC1 ? 3 : 1);
-      for (int c = off; c < off + w; c++) p.chan_mask[n][split == 2 ? (k & 1) : 0] |= 1ull << c;
-    }
+    if ((want >= 2 && want <= 4 || want == 8) && fused_smem(p, want) <= cap) nwg = want;
   }
   const size_t smem = fused_smem(p, nwg);
   if (smem > cap) return fail(NTBC_EINVAL, "model needs %zu B of shared memory (> %zu)", smem, cap);
   int grid = (p.n_units + nwg - 1) / nwg;
   if (grid > sms) grid = sms;
   if (grid < 1) grid = 1;
-#define NTBC_LAUNCH(HH, NW, SP) \
-  return dump ? launch_fused_t<HH, NW, SP, true>(p, smem, grid, st) : launch_fused_t<HH, NW, SP, false>(p, smem, grid, st);
-#define NTBC_DISPATCH(HH)                                     \
-  if (a.hidden == HH) {                                       \
-    if (split == 2 && HH >= 32) {                             \
-      if (nwg == 3) { NTBC_LAUNCH(HH, 3, (HH >= 32 ? 2 : 1)) } \
-      NTBC_LAUNCH(HH, 2, (HH >= 32 ? 2 : 1))                  \
-    }                                                         \
-    if (nwg == 8) { NTBC_LAUNCH(HH, 8, 1) }                   \
-    if (nwg == 6) { NTBC_LAUNCH(HH, 6, 1) }                   \
-    if (nwg == 5) { NTBC_LAUNCH(HH, 5, 1) }                   \
-    if (nwg == 4) { NTBC_LAUNCH(HH, 4, 1) }                   \
-    if (nwg == 3) { NTBC_LAUNCH(HH, 3, 1) }                   \
-    NTBC_LAUNCH(HH, 2, 1)                                     \
+#define NTBC_DISPATCH(HH)                                                                        \
+  if (a.hidden == HH) {                                                                          \
+    if (nwg == 8) return dump ? launch_fused_t<HH, 8, true>(p, smem, grid, st)                   \
+                              : launch_fused_t<HH, 8, false>(p, smem, grid, st);                 \
+    if (nwg == 4) return dump ? launch_fused_t<HH, 4, true>(p, smem, grid, st)                   \
+                              : launch_fused_t<HH, 4, false>(p, smem, grid, st);                 \
+    if (nwg == 3) return dump ? launch_fused_t<HH, 3, true>(p, smem, grid, st)                   \
+                              : launch_fused_t<HH, 3, false>(p, smem, grid, st);                 \
+    return dump ? launch_fused_t<HH, 2, true>(p, smem, grid, st) : launch_fused_t<HH, 2, false>(p, smem, grid, st); \
   }
   NTBC_DISPATCH(16)
   NTBC_DISPATCH(32)
   NTBC_DISPATCH(64)
-#undef NTBC_LAUNCH
 #undef NTBC_DISPATCH
   return fail(NTBC_EINVAL, "unsupported hidden width");
 }
@@ -350,18 +330,23 @@ bool stream_waits_supported(int device) {
   return ok;
 }
 
+bool create_copy_streams(ntbc_model_s* m) {
+  for (int i = 0; i < kCopyStreams; i++)
+    if (cudaStreamCreateWithFlags(&m->copy_stream[i], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&m->copy_done[i], cudaEventDisableTiming) != cudaSuccess)
+      return false;
+  return true;
+}
+
 // streams, events, progress counters and the second weight slot of the pipelined host path
 // (allocated once per model; on failure the host path falls back to serial copies on `stream`)
 bool ensure_copy_state(ntbc_model_s* m) {
   if (m->d_progress) return true;
   const unsigned f = cudaEventDisableTiming;
   bool ok = cudaMalloc(&m->slot_blob[1], m->blob_cap) == cudaSuccess &&
-            cudaMalloc(&m->slot_img[1], m->img_bytes) == cudaSuccess &&
-            cudaMemset(m->slot_img[1], 0, m->img_bytes) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
+            create_copy_streams(m) &&
             cudaStreamCreateWithFlags(&m->upload_stream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&m->copy_start, f) == cudaSuccess &&
-            cudaEventCreateWithFlags(&m->copy_done, f) == cudaSuccess &&
             cudaEventCreateWithFlags(&m->uploaded, f) == cudaSuccess &&
             cudaEventCreateWithFlags(&m->slot_free[0], f) == cudaSuccess &&
             cudaEventCreateWithFlags(&m->slot_free[1], f) == cudaSuccess &&
@@ -375,7 +360,6 @@ bool ensure_copy_state(ntbc_model_s* m) {
     return false;
   }
   m->slot_blob[0] = m->d_blob;
-  m->slot_img[0] = m->d_img;
   m->cur = 0;
   return true;
 }
@@ -405,13 +389,13 @@ ntbc_status ntbc_load_model(const void* blob, size_t nbytes, int cuda_device, nt
   m->device = cuda_device;
   m->arch = a;
   layout_nets(m);
-  if (cudaMalloc(&m->d_blob, al16(nbytes)) != cudaSuccess || cudaMalloc(&m->d_img, m->img_bytes) != cudaSuccess) {
+  if (cudaMalloc(&m->d_blob, al16(nbytes)) != cudaSuccess) {
     cudaGetLastError();
     ntbc_free_model(m);
-    return fail(NTBC_ENOMEM, "device allocation of %zu bytes failed", nbytes + m->img_bytes);
+    return fail(NTBC_ENOMEM, "device allocation of %zu bytes failed", nbytes);
   }
   m->blob_cap = al16(nbytes);
-  cudaMemset(m->d_img, 0, m->img_bytes);
+  if (cudaMalloc(&m->d_sched, kSchedRing * sizeof(int)) != cudaSuccess) { cudaGetLastError(); m->d_sched = nullptr; }
   st = upload(m, blob, nbytes, 0);
   if (st == NTBC_OK && cudaDeviceSynchronize() != cudaSuccess) st = fail(NTBC_ECUDA, "model upload: %s", cudaGetErrorString(cudaGetLastError()));
   if (st) { ntbc_free_model(m); return st; }
@@ -445,7 +429,7 @@ ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out) {
   out->texel_levels = a.levels[1];
   out->texel_coarsest = a.coarsest[1];
   out->features = a.F;
-  out->device_bytes = (m->blob_cap + m->img_bytes) * (m->slot_blob[1] ? 2 : 1) + m->scratch_bytes;
+  out->device_bytes = m->blob_cap * (m->slot_blob[1] ? 2 : 1) + m->scratch_bytes;
   return NTBC_OK;
 }
 
@@ -453,17 +437,18 @@ void ntbc_free_model(ntbc_model m) {
   if (!m) return;
   DevGuard dg(m->device);
   cudaFree(m->slot_blob[0] ? m->slot_blob[0] : m->d_blob);
-  cudaFree(m->slot_img[0] ? m->slot_img[0] : m->d_img);
   cudaFree(m->d_scratch);
+  cudaFree(m->d_sched);
   cudaFree(m->d_progress);
   if (m->copy_start) cudaEventDestroy(m->copy_start);
-  if (m->copy_done) cudaEventDestroy(m->copy_done);
-  if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  for (int i = 0; i < kCopyStreams; i++) {
+    if (m->copy_stream[i]) cudaStreamDestroy(m->copy_stream[i]);
+    if (m->copy_done[i]) cudaEventDestroy(m->copy_done[i]);
+  }
   for (int i = 0; i < 2; i++) if (m->slot_free[i]) cudaEventDestroy(m->slot_free[i]);
   if (m->uploaded) cudaEventDestroy(m->uploaded);
   if (m->upload_stream) cudaStreamDestroy(m->upload_stream);
   cudaFree(m->slot_blob[1]);
-  cudaFree(m->slot_img[1]);
   delete m;
 }
 
@@ -483,7 +468,7 @@ ntbc_status ntbc_decode_material(const ntbc_model* models, int n_models, int wid
   }
   int t = 0;
   for (int i = 0; i < n_models; i++) {
-    const ntbc_model_s* m = models[i];
+    ntbc_model_s* m = models[i];
     DevGuard dg(m->device);
     FusedParams p{};
     p.W = width; p.H = height; p.row_begin = r0; p.row_end = r1;
@@ -535,8 +520,12 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
     for (int k = 0; k < n_tex; k++) p.out[k] = (uint64_t*)(m->d_scratch + k * plane);
     // row chunks for the pipelined copy-back: ~16 chunks of whole block rows
     const int upr = (BW + kUnitBlocks - 1) / kUnitBlocks;
-    const int rows_per_chunk = std::max(1, (BH + 15) / 16);  // 16 chunks: best of 4/8/16/32 measured
-    const int n_chunks = (BH + rows_per_chunk - 1) / rows_per_chunk;
+    // 1/16 of the rows per chunk, except the last three such chunks, which are split 4 ways: their
+    // rows finish last, and only the final chunk's copy is exposed after the kernel
+    // 8 chunks (measured 2/4/8/16/32 -> 8 best; each stream wait + its copies has a fixed cost)
+    const int big = std::max(1, (BH + 7) / 8);
+    const int n_chunks = (BH + big - 1) / big;
+    auto chunk_rows = [&](int c, int& r0, int& r1) { r0 = c * big; r1 = std::min(BH, r0 + big); };
     const bool pipelined = stream_waits_supported(m->device) && n_chunks <= kMaxChunks && ensure_copy_state(m);
     if (!pipelined) {
       st = ntbc_model_upload_async(m, blobs[i], blob_sizes[i], stream);
@@ -552,7 +541,6 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
       m->arch = a;
       m->cur = s;
       m->d_blob = m->slot_blob[s];
-      m->d_img = m->slot_img[s];
       CUDA_TRY(cudaStreamWaitEvent(m->upload_stream, m->slot_free[s], 0));
       st = upload(m, blobs[i], blob_sizes[i], m->upload_stream);
       if (st) return st;
@@ -561,11 +549,11 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
     }
     if (pipelined) {
       p.progress = m->d_progress;
-      p.chunk_units = rows_per_chunk * upr;
+      p.chunk_rows = big;
     }
     if (pipelined) {  // copy stream: ordered after the upload and whatever precedes it on `stream`
       CUDA_TRY(cudaEventRecord(m->copy_start, cs));
-      CUDA_TRY(cudaStreamWaitEvent(m->copy_stream, m->copy_start, 0));
+      for (int i = 0; i < kCopyStreams; i++) CUDA_TRY(cudaStreamWaitEvent(m->copy_stream[i], m->copy_start, 0));
     }
     st = launch_fused(m, p, false, cs);
     if (st) return st;
@@ -576,17 +564,21 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
     } else {
       // chunk c's copies wait until all units of chunk c have been published by the running kernel
       for (int c = 0; c < n_chunks; c++) {
-        const int r0 = c * rows_per_chunk, r1 = std::min(BH, r0 + rows_per_chunk);
+        int r0, r1;
+        chunk_rows(c, r0, r1);
         m->progress_target[c] += (unsigned long long)(r1 - r0) * upr;
-        if (g_wait64((CUstream)m->copy_stream, (CUdeviceptr)(m->d_progress + c), m->progress_target[c],
+        cudaStream_t xs = m->copy_stream[c % kCopyStreams];
+        if (g_wait64((CUstream)xs, (CUdeviceptr)(m->d_progress + c), m->progress_target[c],
                      CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
           return fail(NTBC_ECUDA, "stream wait on progress counter failed");
         for (int k = 0; k < n_tex; k++)
           CUDA_TRY(cudaMemcpyAsync((uint8_t*)host_out[t + k] + r0 * row_bytes, (const uint8_t*)p.out[k] + r0 * row_bytes,
-                                   (size_t)(r1 - r0) * row_bytes, cudaMemcpyDeviceToHost, m->copy_stream));
+                                   (size_t)(r1 - r0) * row_bytes, cudaMemcpyDeviceToHost, xs));
       }
-      CUDA_TRY(cudaEventRecord(m->copy_done, m->copy_stream));
-      CUDA_TRY(cudaStreamWaitEvent(cs, m->copy_done, 0));  // the caller's stream sees the finished copies
+      for (int i = 0; i < kCopyStreams; i++) {   // the caller's stream sees every finished copy
+        CUDA_TRY(cudaEventRecord(m->copy_done[i], m->copy_stream[i]));
+        CUDA_TRY(cudaStreamWaitEvent(cs, m->copy_done[i], 0));
+      }
     }
     t += n_tex;
   }

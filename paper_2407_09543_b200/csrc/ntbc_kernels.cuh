@@ -4,7 +4,7 @@
 //       endpoint quantization, palettes, per-texel argmax, warp-ballot bit packing (a5-a8);
 //   (2) pack_kernel: rows a5-a8 standalone, fed fp32 MLP outputs (HBM-bound);
 //   (3) decode_bc_kernel: BC1/BC4 -> fp32 texels (row a9, verification).
-// Plus relayout_kernel (model upload) and mma_probe_kernel (pins the tensor-core summation, R10).
+// Plus mma_probe_kernel (pins the tensor-core summation, R10).
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
@@ -18,9 +18,7 @@ constexpr int kMaxTex = 8;
 constexpr int kMaxLevels = 8;
 constexpr int kUnitBlocks = 128;  // block positions per work unit = rows of one endpoint MMA tile
 constexpr int kFmtBC1 = 1;
-#ifndef NTBC_PREFETCH_MAXNWG
-#define NTBC_PREFETCH_MAXNWG 4
-#endif
+
 constexpr int kUnormBytes = 1536;  // 352 fp32 UNORM expansion values (q/31, q/63, q/255) + 32 BC4 weights
 
 struct GridLevel {
@@ -31,15 +29,15 @@ struct GridLevel {
 };
 
 struct NetLayout {
-  uint32_t img_off;       // byte offset of this net's operand image inside Model::d_img
-  uint32_t img_bytes;
+  uint32_t img_bytes;     // shared-memory operand image of this net (built by the fused kernel)
   uint32_t layer_off[4];  // byte offset of layer l's B operand [N_l][K_l] inside the net image
+  uint32_t w_off[4], b_off[4];  // blob byte offsets of layer l's fp16 W [in][out] and bias [out]
+  int kin[4], nout[4];    // layer l's input / output widths
   int n_out, n_out16;
 };
 
 struct FusedParams {
   const uint8_t* blob;    // device copy of the .ntbc blob (grid payloads are read from here)
-  const uint8_t* img;     // device operand images (both nets, tcgen05 K-major layout, bias folded)
   GridLevel lv[2][kMaxLevels];
   int levels[2];
   NetLayout net[2];
@@ -52,9 +50,9 @@ struct FusedParams {
   uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
   uint32_t debug_flags;         // bit 1: grid-feature dump (ntbc_debug_features)
   int k23;                      // = 1 << 23 (run-time constant, see selu2_h2)
-  uint64_t chan_mask[2][2];     // [net][half]: output channels whose sigmoid this half computes (SPLIT)
   unsigned long long* progress; // optional: per-chunk count of finished units (pipelined D2H, see ntbc_api.cu)
-  int chunk_units;              // units per progress chunk
+  int chunk_rows;               // block rows per progress chunk
+  int* next_unit;               // optional: dynamic unit counter (zeroed before the launch)
 };
 
 // ---------------------------------------------------------------- a1-a2: coordinates + grid encode
@@ -132,52 +130,58 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, in
 }
 
 // ---------------------------------------------------------------- kernel (1): fused decode
-// One CTA per SM, NWG independent work groups of SPLIT x 4 warps.  A work group owns 64 TMEM columns,
-// an A-operand buffer and a palette buffer, and loops over work units of 128 block positions of one
-// block row: one endpoint tile (128 blocks) then up to 16 colour tiles (8 blocks = 128 texels).
-// Row r of a tile lives in TMEM lane r, so it is handled by the warps with (warp % 4) == r / 32; with
-// SPLIT = 2 two warps share each lane quarter and split the work of a row: grid levels 0-3 / 4-7,
-// hidden columns [0, H/2) / [H/2, H), textures k % 2 == 0 / 1.  More warps per SM hide the latency of
-// the dependent epilogue chains at the same register file.
-template <int H, int NWG, int SPLIT, bool DUMP>
-__global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
-  constexpr int GT = 128 * SPLIT;   // threads per work group
-  constexpr int HC = H / SPLIT;     // hidden columns per thread
-  static_assert(HC % 16 == 0, "hidden columns per thread must be a multiple of 16");
+// One CTA per SM, NWG independent 128-thread work groups (8 for H = 64: 64 registers per thread, all
+// 512 TMEM columns); each work group owns 64 TMEM columns, an A-operand buffer and the BC word headers
+// of its unit, and loops over work units of 128 block positions of one block row: one endpoint tile
+// (128 blocks) then up to 16 colour tiles (8 blocks = 128 texels).  More independent groups per SM
+// hide more of the dependent epilogue latency.  Units are claimed from a global
+// counter (dynamic scheduling) so they finish in row order (pipelined copy-back, ntbc_api.cu).
+template <int H, int NWG, bool DUMP>
+__global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int tid = threadIdx.x, wg = tid / GT, gt = tid % GT, warp = tid >> 5, lane = tid & 31;
-  const int r = gt & 127, half = gt >> 7;   // tile row (= TMEM lane) and share of the row's work
-  const bool leader = gt == 0;
+  const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5, lane = tid & 31;
 
   // ---- carve shared memory
   uint8_t* img_e = smem;                                          // endpoint net operand image
   uint8_t* img_c = smem + p.net[0].img_bytes;                     // colour net operand image
   uint8_t* ones = img_c + p.net[1].img_bytes;                     // [128][16] K-major, column 0 = 1.0
-  float* unorm = reinterpret_cast<float*>(ones + 4096);            // q/31 [32], q/63 [64], q/255 [256]
+  float* unorm = reinterpret_cast<float*>(ones + 4096);           // q/31 [32], q/63 [64], q/255 [256], BC4 weights
   uint8_t* wg_base = ones + 4096 + kUnormBytes + wg * (p.a_bytes + p.pal_bytes);
   uint8_t* A = wg_base;                                           // [128][H] K-major fp16 / fp32 staging
   float* stage = reinterpret_cast<float*>(A);                     // [ch][128] fp32 (after the last MMA)
   uint32_t* hdrs = reinterpret_cast<uint32_t*>(wg_base + p.a_bytes);  // [tex][128 blocks] BC word low bits
   uint64_t* bars = reinterpret_cast<uint64_t*>(ones + 4096 + kUnormBytes + NWG * (p.a_bytes + p.pal_bytes));
-  uint64_t* bar_w = bars;                                         // weights landed
-  uint64_t* bar_mma = bars + 1 + wg;                              // this work group's MMA completion
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + NWG);
+  uint64_t* bar_mma = bars + wg;                                  // this work group's MMA completion
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
+  int* next_slot = reinterpret_cast<int*>(tmem_slot + 1) + wg;    // dynamic scheduling: this group's next unit
 
   if (tid == 0) {
-    mbar_init(bar_w, 1);
-    for (int g = 0; g < NWG; g++) mbar_init(bars + 1 + g, 1);
+    for (int g = 0; g < NWG; g++) mbar_init(bars + g, 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, NWG <= 2 ? 128 : NWG <= 4 ? 256 : 512);
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
 
-  // ---- stage both nets' operand images with the bulk-copy (TMA) engine
-  if (tid == 0) {
-    mbar_arrive_expect_tx(bar_w, p.net[0].img_bytes + p.net[1].img_bytes);
-    bulk_g2s(img_e, p.img + p.net[0].img_off, p.net[0].img_bytes, bar_w);
-    bulk_g2s(img_c, p.img + p.net[1].img_off, p.net[1].img_bytes, bar_w);
+  // ---- operand images of both nets, built from the blob's row-major fp16 weights: row n of layer l's
+  //      B operand = output n, K-major core-matrix layout, bias at k = kin16 (read against the ones tile)
+#pragma unroll 1
+  for (int n = 0; n < 2; n++) {
+    uint8_t* img = n == 0 ? img_e : img_c;
+#pragma unroll 1
+    for (int l = 0; l < 4; l++) {
+      const NetLayout& L = p.net[n];
+      const int kin = L.kin[l], nout = L.nout[l], kin16 = l == 0 ? 16 : H, npad = l < 3 ? H : L.n_out16;
+      const int K_B = kin16 + 16;
+      const __half* W = reinterpret_cast<const __half*>(p.blob + L.w_off[l]);
+      const __half* bias = reinterpret_cast<const __half*>(p.blob + L.b_off[l]);
+      uint8_t* dst = img + L.layer_off[l];
+      for (int t = tid; t < npad * K_B; t += NWG * 128) {
+        const int k = t / npad, o = t - k * npad;   // o fastest: coalesced reads of W[k][o]
+        __half v = __ushort_as_half((unsigned short)0);
+        if (o < nout && k < kin) v = W[(size_t)k * nout + o];
+        else if (o < nout && k == kin16) v = bias[o];
+        *reinterpret_cast<__half*>(dst + kmajor_offset(o, k, K_B)) = v;
+      }
+    }
   }
   if (tid < 128) {  // the constant ones tile used to fold the bias into the MMA
     const uint4 c0 = make_uint4(0x3C00u, 0u, 0u, 0u), z = make_uint4(0u, 0u, 0u, 0u);
@@ -189,8 +193,9 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
                                                              : __fdiv_rn((float)(i - 96), 255.0f);
   if (tid < 32) unorm[352 + tid] = bc4_weight(tid);   // BC4 interpolation weights per mode
   fence_async_smem();
-  mbar_wait(bar_w, 0);
   __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
 
   const uint32_t tm = tmem_base + (uint32_t)(wg * 64);                    // D columns of this group
   const uint32_t tm_row = tm + ((uint32_t)(32 * (warp & 3)) << 16);       // this warp's TMEM lanes
@@ -198,26 +203,20 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
   const uint32_t img_base[2] = {smem_u32(img_e), smem_u32(img_c)};
   const int bar_id = 1 + wg;
   uint32_t phase = 0;
-  // textures (and hence output channels) handled by this thread
-  auto mine = [&](int k) { return SPLIT == 1 || (k % SPLIT) == half; };
 
-  // 16 grid features of row r (levels coarse->fine, 2 per level, R3) -> fp16 -> A columns 0..15;
-  // with SPLIT = 2 this thread does levels [8/SPLIT * half, ...) (one 16-B store)
+  // 16 grid features of row r (levels coarse->fine, 2 per level, R3) -> fp16 -> A columns 0..15
   auto features = [&](int g, float pu, float pv, float* dump) {
-    constexpr int LPT = kMaxLevels / SPLIT;
-    uint32_t hv[LPT];
+    uint32_t hv[kMaxLevels];
 #pragma unroll
-    for (int i = 0; i < LPT; i++) {
-      const int l = LPT * half + i;
+    for (int l = 0; l < kMaxLevels; l++) {
       float f0, f1;   // all levels unconditionally: unused ones are set up to return +0 (launch_fused)
       f2unpack(level_lookup2(p.blob, p.lv[g][l], pu, pv), f0, f1);
       if (dump) { dump[2 * l] = f0; dump[2 * l + 1] = f1; }
       const __half2 v = __floats2half2_rn(f0, f1);
-      hv[i] = *reinterpret_cast<const uint32_t*>(&v);
+      hv[l] = *reinterpret_cast<const uint32_t*>(&v);
     }
-#pragma unroll
-    for (int i = 0; i < LPT; i += 4)
-      *reinterpret_cast<uint4*>(A + kmajor_offset(r, 2 * (LPT * half + i), H)) = make_uint4(hv[i], hv[i + 1], hv[i + 2], hv[i + 3]);
+    *reinterpret_cast<uint4*>(A + kmajor_offset(r, 0, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    *reinterpret_cast<uint4*>(A + kmajor_offset(r, 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
   };
 
   // run the 4-layer MLP of net `n` on the A rows already written; leaves the output layer in TMEM
@@ -226,46 +225,43 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
     for (int l = 0; l < 4; l++) {
       fence_async_smem();
       tc_fence_before();
-      named_bar_sync(bar_id, GT);
-      if (leader) {
+      named_bar_sync(bar_id, 128);
+      if (r == 0) {
         tc_fence_after();
         const int kin16 = l == 0 ? 16 : H;
         const int N = l < 3 ? H : p.net[n].n_out16;
         issue_layer(tm, a_base, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
         mma_commit(bar_mma);
       }
-      if (leader) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
-      named_bar_sync(bar_id, GT);
+      if (r == 0) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
+      named_bar_sync(bar_id, 128);
       phase ^= 1u;
       tc_fence_after();
       if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10), 16 columns at a time
-        const uint32_t t0 = tm_row + half * HC;
-        constexpr bool PF = NWG <= NTBC_PREFETCH_MAXNWG;   // prefetch the next chunk (needs 16 more registers)
+        constexpr bool PF = NWG <= 4;   // prefetch the next chunk (16 more registers than NWG 8 has)
         uint32_t buf[2][16];
-        tmem_ld16p(t0, buf[0]);
+        tmem_ld16p(tm_row, buf[0]);
         tmem_wait_ld16(buf[0]);
 #pragma unroll
-        for (int c = 0; c < HC / 16; c++) {
+        for (int c = 0; c < H / 16; c++) {
           if (!PF && c > 0) {
-            tmem_ld16p(t0 + c * 16, buf[c & 1]);
+            tmem_ld16p(tm_row + c * 16, buf[c & 1]);
             tmem_wait_ld16(buf[c & 1]);
           }
-          if (PF && c + 1 < HC / 16) tmem_ld16p(t0 + (c + 1) * 16, buf[(c + 1) & 1]);   // prefetch next chunk
+          if (PF && c + 1 < H / 16) tmem_ld16p(tm_row + (c + 1) * 16, buf[(c + 1) & 1]);
           uint32_t hv[8];
 #pragma unroll
           for (int j = 0; j < 8; j++)
             hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]), p.k23);
-          const int col = half * HC + c * 16;
-          *reinterpret_cast<uint4*>(A + kmajor_offset(r, col, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-          *reinterpret_cast<uint4*>(A + kmajor_offset(r, col + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
-          if (PF && c + 1 < HC / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
+          *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+          *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+          if (PF && c + 1 < H / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
         }
       }
     }
   };
-  // output layer epilogue: sigmoid of this thread's output channels (pairs) -> fp32 staging [ch][128]
+  // output layer epilogue: sigmoid of the output channels (pairs) -> fp32 staging [ch][128]
   auto stage_outputs = [&](int n) {
-    const uint64_t own = DUMP ? ~0ull : p.chan_mask[n][SPLIT == 1 ? 0 : half];
     const int no = p.net[n].n_out;
 #pragma unroll 1
     for (int c16 = 0; c16 < no; c16 += 16) {
@@ -275,7 +271,7 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
 #pragma unroll
       for (int j = 0; j < 16; j += 2) {
         const int ch = c16 + j;
-        if (ch < no && ((own >> ch) & 3ull)) {
+        if (ch < no) {
           float s0, s1;
           sigmoid2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), s0, s1);
           stage[ch * 128 + r] = s0;
@@ -286,14 +282,17 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
   };
 
 #pragma unroll 1
-  for (int u = blockIdx.x * NWG + wg; u < p.n_units; u += gridDim.x * NWG) {
+  for (int u = blockIdx.x * NWG + wg; u < p.n_units;) {
     const int by = p.row_begin + u / p.units_per_row;
     const int bx0 = (u % p.units_per_row) * kUnitBlocks;
     const int nvalid = min(kUnitBlocks, p.BW - bx0);
     const size_t out_row = (size_t)(by - p.row_begin) * p.BW;
 
     // ================= endpoint tile: row r = block (bx0 + r, by)  (rows a1-a3, a5-a6)
-    named_bar_sync(bar_id, GT);  // previous tile's readers of A / staging / palettes are done
+    named_bar_sync(bar_id, 128);  // previous tile's readers of A / staging / headers are done
+    // dynamic scheduling (p.next_unit): claim the group's next unit now; it is read at the end of this
+    // unit, after the MLP's barriers have ordered the store before every reader
+    if (p.next_unit && r == 0) *next_slot = atomicAdd(p.next_unit, 1) + (int)gridDim.x * NWG;
     {
       const float s = __fdiv_rn(__fadd_rn((float)min(bx0 + r, p.BW - 1), 0.5f), (float)p.BW);
       const float t = __fdiv_rn(__fadd_rn((float)by, 0.5f), (float)p.BH);
@@ -303,12 +302,11 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
     run_mlp(0);
     stage_outputs(0);
     if (DUMP) {
-      if (half == 0 && r < nvalid && !(p.debug_flags & 2))
+      if (r < nvalid && !(p.debug_flags & 2))
         for (int ch = 0; ch < p.net[0].n_out; ch++)
           p.dump_ep[(out_row + bx0 + r) * p.net[0].n_out + ch] = stage[ch * 128 + r];
     } else {
       for (int k = 0; k < p.n_tex; k++) {
-        if (!mine(k)) continue;
         const int eo = p.ep_off[k];
         if (p.fmt[k] == kFmtBC1) {  // BC word header after quantization and the 4-colour-mode swap (R11, R12)
           float ep[6];
@@ -327,7 +325,7 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
     for (int j = 0; j < kUnitBlocks / 8 && 8 * j < nvalid; j++) {
       const int b = 8 * j + (r >> 4), i = r & 15;
       const int bx = bx0 + b, x = 4 * min(bx, p.BW - 1) + (i & 3), y = 4 * by + (i >> 2);
-      named_bar_sync(bar_id, GT);
+      named_bar_sync(bar_id, 128);
       {
         const float pu = __fdiv_rn(__fadd_rn((float)x, 0.5f), (float)p.W);
         const float pv = __fdiv_rn(__fadd_rn((float)y, 0.5f), (float)p.H);
@@ -338,12 +336,11 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
       run_mlp(1);
       stage_outputs(1);
       if (DUMP) {
-        if (half == 0 && b < nvalid && !(p.debug_flags & 2))
+        if (b < nvalid && !(p.debug_flags & 2))
           for (int ch = 0; ch < p.net[1].n_out; ch++)
             p.dump_col[(((size_t)(y - 4 * p.row_begin)) * p.W + x) * p.net[1].n_out + ch] = stage[ch * 128 + r];
       } else {
         for (int k = 0; k < p.n_tex; k++) {
-          if (!mine(k)) continue;
           const int co = p.col_off[k];
           const uint32_t hdr = hdrs[k * 128 + b];
           uint64_t word;
@@ -366,12 +363,14 @@ __global__ void __launch_bounds__(NWG * 128 * SPLIT, 1) fused_decode_kernel(cons
       }
     }
     if (!DUMP && p.progress) {  // publish the finished unit: group barrier, then one system-scope release
-      named_bar_sync(bar_id, GT);
-      if (leader) {
+      named_bar_sync(bar_id, 128);
+      if (r == 0) {
         __threadfence_system();   // the consumer is the copy engine (measured: same cost as a gpu fence)
-        atomicAdd(p.progress + u / p.chunk_units, 1ull);
+        const int row = u / p.units_per_row;
+        atomicAdd(p.progress + row / p.chunk_rows, 1ull);
       }
     }
+    u = p.next_unit ? *next_slot : u + (int)gridDim.x * NWG;
   }
 
   __syncthreads();
@@ -469,21 +468,6 @@ __global__ void __launch_bounds__(256) decode_bc_kernel(const uint64_t* __restri
       out[t] = v;
     }
   }
-}
-
-// ---------------------------------------------------------------- model upload: operand relayout
-// B operand of one layer: [Npad][K_B] K-major (sm100.cuh kmajor_offset), K_B = kin16 + 16,
-// W[k][n] for k < kin, n < nout; bias in column kin16; zeros elsewhere.
-__global__ void relayout_kernel(const __half* __restrict__ W, const __half* __restrict__ b, int kin, int nout,
-                                int kin16, int npad, uint8_t* __restrict__ dst) {
-  const int K_B = kin16 + 16;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= npad * K_B) return;
-  const int n = t / K_B, k = t % K_B;
-  __half v = __float2half_rn(0.0f);
-  if (n < nout && k < kin) v = W[(size_t)k * nout + n];
-  else if (n < nout && k == kin16) v = b[n];
-  *reinterpret_cast<__half*>(dst + kmajor_offset(n, k, K_B)) = v;
 }
 
 // ---------------------------------------------------------------- tensor-core summation probe (R10)

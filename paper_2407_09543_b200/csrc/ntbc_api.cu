@@ -267,12 +267,16 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t cap = 227 * 1024;
-  // work groups per CTA: more independent groups hide more latency (C3: NWG 4 -> 2.70 ms, 6 -> 2.65 with
-  // 8% wave-quantisation loss, 8 -> 2.46); 5 and 6 quantise badly on power-of-two unit counts
-  // (measured for H = 64 only; the H = 32 model of C2 runs 0.19 ms at NWG 4 and 0.34 ms at 8)
+  // work groups per CTA: more independent groups per SM hide more latency (C3: NWG 4 -> 2.70 ms,
+  // 6 -> 2.65 with 8% wave-quantisation loss, 8 -> 2.46) but each group's unit takes ~1.8x longer, so
+  // 8 groups pay only with at least two full waves of units (C2, 512 units: NWG 4 = 0.19 ms on 128
+  // SMs in one wave, NWG 8 = 0.34 ms on 64 SMs); 5 and 6 quantise badly on power-of-two unit counts
+  int dev0 = 0, sms0 = 148;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
   int nwg = 2;
   for (int w : {8, 4, 3})
-    if ((w != 8 || a.hidden >= 64) && fused_smem(p, w) <= cap) { nwg = w; break; }
+    if ((w != 8 || p.n_units >= 2 * 8 * sms0) && fused_smem(p, w) <= cap) { nwg = w; break; }
   if (const char* e = getenv("NTBC_NWG")) {  // measurement override (bench sweeps); clamped to what fits
     const int want = atoi(e);
     if ((want >= 2 && want <= 4 || want == 8) && fused_smem(p, want) <= cap) nwg = want;

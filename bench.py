@@ -142,8 +142,9 @@ def run_reference(args, rank, world):
     import oracle
     om = oracle.Model(synth.model_blob(args.config))
     threads = os.cpu_count() or 1
-    # size each step to about 1-2 s of host time: one block row per step by default
-    rows = 1
+    # each step: one full-width block row per host thread (the oracle parallelises over rows), about
+    # 2 s of host time on 16 cores, so that every core is busy and K steps end within minutes
+    rows = max(1, min(threads, H // 4))
     for _ in range(args.warmup):
         om.decode_material(W, H, 0, rows, nthreads=threads)
     t0 = time.perf_counter()

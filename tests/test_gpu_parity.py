@@ -174,7 +174,7 @@ def test_c2_full_material_words(ntbc):
         assert np.array_equal(u64(outs[k]), ref[k]), k
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("cfg", [3, 4, 6])
 def test_4k_sampled_rows(ntbc, cfg):
     W, H, _ = synth.config_shape(cfg)
     check_material(ntbc, cfg, W, H, [(0, 1), (517, 518), (H // 4 - 1, H // 4)])
@@ -219,6 +219,24 @@ def test_conservative_pair_and_mismatch_rules(ntbc):
         torch.cuda.synchronize()
         for k in range(6):
             assert np.array_equal(host[k].numpy().view(np.uint64), ref[k])
+
+
+def test_tab1_conservative_pair_4k_sampled_rows(ntbc):
+    """The paper's conservative workload (tools/tab1.py) at full size: an all-BC1 model and an
+    all-BC4 model of the paper architecture decoded in one call; sampled rows of all 6 textures."""
+    W, H = 4096, 4096
+    blobs = [synth.serialize(synth.random_model(synth.ModelSpec([synth.BC1] * 2), 101)),
+             synth.serialize(synth.random_model(synth.ModelSpec([synth.BC4] * 4), 102))]
+    ms = [ntbc.Model(b) for b in blobs]
+    outs = ntbc.decode_material(ms, W, H)
+    t = 0
+    for b in blobs:
+        om = oracle.Model(b)
+        for r0, r1 in ((0, 1), (H // 4 - 1, H // 4)):
+            ref = om.decode_material(W, H, r0, r1)
+            for k in range(len(ref)):
+                assert np.array_equal(u64(outs[t + k])[r0:r1], ref[k])
+        t += om.n_tex
 
 
 def test_row_shards_union_equals_full(ntbc):

@@ -62,6 +62,9 @@ def lib():
             "o_argmin_bc4": (i32, [f32, vp]),
             "o_encode_bc1": (u64, [vp, vp]),
             "o_encode_bc4": (u64, [vp, vp]),
+            "o_quantize_weight": (i32, [f32, i32, i32]),
+            "o_encode_bc1_naive": (u64, [vp, vp]),
+            "o_encode_bc4_naive": (u64, [vp, vp]),
             "o_decode_block": (None, [u64, i32, vp]),
             "o_decode_material": (None, [vp, i32, i32, i32, i32, vp, i32]),
             "o_mlp_outputs": (None, [vp, i32, i32, i32, i32, vp, vp, i32]),
@@ -95,12 +98,13 @@ class Model:
         if rc != 0:
             raise ValueError(f"oracle: bad model blob (rc={rc})")
         self.h = h
-        info = np.zeros(16, np.int32)
+        info = np.zeros(17, np.int32)
         lib().o_model_info(h, _p(info))
         self.n_tex = int(info[0])
         self.fmts = [int(x) for x in info[1:1 + self.n_tex]]
         self.hidden, self.n_e, self.n_c = int(info[9]), int(info[10]), int(info[11])
         self.block_levels, self.texel_levels = int(info[12]), int(info[14])
+        self.naive = bool(info[16])
 
     def __del__(self):
         try:
@@ -199,6 +203,34 @@ def encode_bc4(ep2, texels16) -> int:
     e = np.ascontiguousarray(ep2, np.float32)
     t = np.ascontiguousarray(texels16, np.float32).reshape(-1)
     return int(lib().o_encode_bc4(_p(e), _p(t)))
+
+
+def rgb565(e3) -> int:
+    e = np.ascontiguousarray(e3, np.float32)
+    return int(lib().o_rgb565(_p(e)))
+
+
+def expand565(c: int) -> np.ndarray:
+    out = np.zeros(3, np.float32)
+    lib().o_expand565(int(c), _p(out))
+    return out
+
+
+def quantize_weight(w: float, fmt: int, mode8: bool = True) -> int:
+    """Naive approach: linear palette index of the nearest palette weight (ties -> lower n)."""
+    return int(lib().o_quantize_weight(float(w), int(fmt), int(bool(mode8))))
+
+
+def encode_bc1_naive(ep6, weights16) -> int:
+    e = np.ascontiguousarray(ep6, np.float32)
+    w = np.ascontiguousarray(weights16, np.float32).reshape(-1)
+    return int(lib().o_encode_bc1_naive(_p(e), _p(w)))
+
+
+def encode_bc4_naive(ep2, weights16) -> int:
+    e = np.ascontiguousarray(ep2, np.float32)
+    w = np.ascontiguousarray(weights16, np.float32).reshape(-1)
+    return int(lib().o_encode_bc4_naive(_p(e), _p(w)))
 
 
 def decode_block(blk: int, fmt: int) -> np.ndarray:

@@ -35,6 +35,7 @@ typedef struct { int levels, coarsest; o_level lv[MAXLV]; } o_grid;
 typedef struct { int n_layers; int dims[8]; const uint16_t* W[7]; const uint16_t* b[7]; } o_mlp;
 struct o_model {
     int n_tex, fmt[MAXTEX], hidden, n_hidden, F;
+    int naive;             /* header variant: 0 NTBC colour network, 1 naive weight network */
     o_grid grid[2];        /* 0 = block grid, 1 = texel grid */
     o_mlp mlp[2];          /* 0 = endpoint net, 1 = colour net */
     uint8_t* blob;         /* private copy; all pointers above point into it */
@@ -60,6 +61,8 @@ int o_model_parse(const void* blob, size_t n, o_model** out) {
     m->grid[0].levels = (int)rd32(b + 56); m->grid[0].coarsest = (int)rd32(b + 60);
     m->grid[1].levels = (int)rd32(b + 64); m->grid[1].coarsest = (int)rd32(b + 68);
     int ep_in = (int)rd32(b + 72), n_e = (int)rd32(b + 76), col_in = (int)rd32(b + 80), n_c = (int)rd32(b + 84);
+    m->naive = (int)rd32(b + 88);
+    if (m->naive != 0 && m->naive != 1) { o_model_free(m); return -2; }
     if (m->n_hidden < 1 || m->n_hidden > 5 || m->F < 1 || m->grid[0].levels < 1 ||
         m->grid[0].levels > MAXLV || m->grid[1].levels < 1 || m->grid[1].levels > MAXLV) { o_model_free(m); return -2; }
     size_t off = 96;
@@ -98,6 +101,7 @@ int o_model_parse(const void* blob, size_t n, o_model** out) {
     }
     int want_e = 0, want_c = 0;
     for (int i = 0; i < m->n_tex; i++) { want_e += m->fmt[i] == BC1 ? 6 : 2; want_c += m->fmt[i] == BC1 ? 3 : 1; }
+    if (m->naive) want_c = m->n_tex;                          /* one weight per texel per texture */
     if (want_e != n_e || want_c != n_c || ep_in != m->grid[0].levels * m->F ||
         col_in != m->grid[1].levels * m->F) { o_model_free(m); return -2; }
     *out = m;
@@ -107,7 +111,8 @@ int o_model_parse(const void* blob, size_t n, o_model** out) {
 void o_model_free(o_model* m) { if (m) { free(m->blob); free(m); } }
 
 void o_model_info(const o_model* m, int* o) {
-    memset(o, 0, 16 * sizeof(int));
+    memset(o, 0, 17 * sizeof(int));
+    o[16] = m->naive;
     o[0] = m->n_tex;
     for (int i = 0; i < m->n_tex; i++) o[1 + i] = m->fmt[i];
     o[9] = m->hidden;
@@ -458,6 +463,47 @@ uint64_t o_encode_bc4(const float ep[2], const float* tx) {
     return w;
 }
 
+/* Naive approach: the weight network's floating-point weight w_f is quantized to the
+   nearest palette weight w_n of the block's format and mode ("quantizes w_f to w_n"; SPEC
+   quantize_weight: minimize |w_f - w_n|, ties -> lower n).  Weights are the fp32 values the palette
+   uses: n/3 (BC1), n/7 (BC4, E0 > E1), (n-1)/5 for linear n = 1..6 (BC4, E0 <= E1: entries 0 and 7
+   are the constants 0 and 1, which carry no weight).  Returns the linear palette index n. */
+int o_quantize_weight(float w, int fmt, int mode8) {
+    int lo = 0, hi = 3;
+    if (fmt == BC4) { lo = mode8 ? 0 : 1; hi = mode8 ? 7 : 6; }
+    int best = lo; float bd = 0.0f;
+    for (int n = lo; n <= hi; n++) {
+        float wn = fmt == BC1 ? (float)n / 3.0f : mode8 ? (float)n / 7.0f : (float)(n - 1) / 5.0f;
+        float d = fabsf(w - wn);
+        if (n == lo || d < bd) { bd = d; best = n; }
+    }
+    return best;
+}
+
+/* BC1: the weights are relative to the predicted endpoint order; when the 4-colour-mode rule swaps
+   the stored endpoints, index n maps to 3 - n (SPEC infer_surfaces "swap + index remap"). */
+uint64_t o_encode_bc1_naive(const float ep[6], const float* w) {
+    uint16_t c0 = o_rgb565(ep), c1 = o_rgb565(ep + 3);
+    int swapped = c0 < c1;
+    if (swapped) { uint16_t t = c0; c0 = c1; c1 = t; }
+    uint64_t blk = (uint64_t)c0 | ((uint64_t)c1 << 16);
+    if (c0 == c1) return blk;                                 /* all codes 0 (R12) */
+    for (int i = 0; i < 16; i++) {
+        int n = o_quantize_weight(w[i], BC1, 0);
+        if (swapped) n = 3 - n;
+        blk |= (uint64_t)MAP1[n] << (32 + 2 * i);
+    }
+    return blk;
+}
+
+uint64_t o_encode_bc4_naive(const float ep[2], const float* w) {
+    uint8_t E0 = o_unorm8(ep[0]), E1 = o_unorm8(ep[1]);       /* mode from stored order, no swap (R13) */
+    const int* map = E0 > E1 ? MAP4_8 : MAP4_6;
+    uint64_t blk = (uint64_t)E0 | ((uint64_t)E1 << 8);
+    for (int i = 0; i < 16; i++) blk |= (uint64_t)map[o_quantize_weight(w[i], BC4, E0 > E1)] << (16 + 3 * i);
+    return blk;
+}
+
 void o_decode_block(uint64_t blk, int fmt, float* out) {
     if (fmt == BC1) {
         uint16_t c0 = (uint16_t)blk, c1 = (uint16_t)(blk >> 16);
@@ -516,13 +562,18 @@ static void block_mlp(const o_model* m, int W, int H, int bx, int by, float* ep,
 /* quantize + palette + index + pack one block position for every texture.
    ep: N_e endpoint outputs; col: 16 texels x N_c colour outputs; head layout R17. */
 static void encode_all(int n_tex, const int* fmts, const float* ep, const float* col, int n_c,
-                       uint64_t* out, size_t plane_stride) {
+                       uint64_t* out, size_t plane_stride, int naive) {
     int eo = 0, co = 0;
     for (int k = 0; k < n_tex; k++) {
         int w = fmts[k] == BC1 ? 3 : 1;
         float tx[48];
-        for (int i = 0; i < 16; i++) for (int c = 0; c < w; c++) tx[i * w + c] = col[i * n_c + co + c];
-        out[(size_t)k * plane_stride] = fmts[k] == BC1 ? o_encode_bc1(ep + eo, tx) : o_encode_bc4(ep + eo, tx);
+        if (naive) {                                          /* weight of texture k = output channel k */
+            for (int i = 0; i < 16; i++) tx[i] = col[i * n_c + k];
+            out[(size_t)k * plane_stride] = fmts[k] == BC1 ? o_encode_bc1_naive(ep + eo, tx) : o_encode_bc4_naive(ep + eo, tx);
+        } else {
+            for (int i = 0; i < 16; i++) for (int c = 0; c < w; c++) tx[i * w + c] = col[i * n_c + co + c];
+            out[(size_t)k * plane_stride] = fmts[k] == BC1 ? o_encode_bc1(ep + eo, tx) : o_encode_bc4(ep + eo, tx);
+        }
         eo += 2 * w; co += w;
     }
 }
@@ -558,7 +609,7 @@ void o_pack(int n_tex, const int* fmts, const float* ep, const float* col, int W
                 memcpy(c16 + i * n_c, col + (y * W + x) * n_c, sizeof(float) * n_c);
             }
             encode_all(n_tex, fmts, ep + ((size_t)r * BW + bx) * n_e, c16, n_c,
-                       out + (size_t)r * BW + bx, (size_t)rows * BW);
+                       out + (size_t)r * BW + bx, (size_t)rows * BW, 0);
         }
 }
 
@@ -570,7 +621,7 @@ void o_decode_material(const o_model* m, int W, int H, int r0, int r1, uint64_t*
         for (int bx = 0; bx < BW; bx++) {
             float ep[64], c16[16 * 32];
             block_mlp(m, W, H, bx, r0 + r, ep, c16);
-            encode_all(m->n_tex, m->fmt, ep, c16, n_c, out + (size_t)r * BW + bx, (size_t)rows * BW);
+            encode_all(m->n_tex, m->fmt, ep, c16, n_c, out + (size_t)r * BW + bx, (size_t)rows * BW, m->naive);
         }
 }
 

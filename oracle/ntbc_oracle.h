@@ -28,8 +28,9 @@ typedef struct o_model o_model;
 int  o_model_parse(const void* blob, size_t nbytes, o_model** out);   /* 0 ok, <0 error */
 void o_model_free(o_model* m);
 /* out[0]=n_tex out[1..8]=fmt out[9]=hidden out[10]=n_e out[11]=n_c
-   out[12]=block_levels out[13]=block_coarsest out[14]=texel_levels out[15]=texel_coarsest */
-void o_model_info(const o_model* m, int* out16);
+   out[12]=block_levels out[13]=block_coarsest out[14]=texel_levels out[15]=texel_coarsest
+   out[16]=variant (0 NTBC colour network, 1 naive weight network) */
+void o_model_info(const o_model* m, int* out17);
 
 /* ---- scalar building blocks ---- */
 float    o_f16_to_f32(uint16_t h);
@@ -74,6 +75,10 @@ int      o_argmin_bc1(const float c[3], float pal[4][3]);      /* Eq.9-10 */
 int      o_argmin_bc4(float c, const float pal[8]);            /* Eq.9-10 */
 uint64_t o_encode_bc1(const float ep[6], const float* texels /* 16 x 3 */);
 uint64_t o_encode_bc4(const float ep[2], const float* texels /* 16 */);
+/* naive approach: nearest palette weight (ties -> lower n), linear index */
+int      o_quantize_weight(float w, int fmt, int mode8);
+uint64_t o_encode_bc1_naive(const float ep[6], const float* weights /* 16 */);
+uint64_t o_encode_bc4_naive(const float ep[2], const float* weights /* 16 */);
 void     o_decode_block(uint64_t blk, int fmt, float* out /* 16 x (3|1) */);
 
 /* ---- whole-material paths ---- */

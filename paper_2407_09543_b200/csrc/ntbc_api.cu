@@ -43,6 +43,7 @@ uint32_t rd32(const uint8_t* p) { uint32_t v; memcpy(&v, p, 4); return v; }
 // Parsed architecture of a .ntbc blob.  Offsets index the blob.
 struct Arch {
   int n_tex, fmt[kMaxTex], hidden, n_hidden, F;
+  int naive;                      // header variant: 0 NTBC colour network, 1 naive weight network
   int levels[2], coarsest[2];
   int dims[2][5];                 // [net][layer boundary]
   size_t level_off[2][kMaxLevels];
@@ -70,11 +71,14 @@ ntbc_status parse(const void* blob, size_t n, Arch& a) {
   a.levels[0] = (int)rd32(b + 56); a.coarsest[0] = (int)rd32(b + 60);
   a.levels[1] = (int)rd32(b + 64); a.coarsest[1] = (int)rd32(b + 68);
   const int ep_in = (int)rd32(b + 72), n_e = (int)rd32(b + 76), col_in = (int)rd32(b + 80), n_c = (int)rd32(b + 84);
+  a.naive = (int)rd32(b + 88);
+  if (a.naive != 0 && a.naive != 1) return fail(NTBC_EFORMAT, "unknown model variant %d", a.naive);
   if (a.hidden != 16 && a.hidden != 32 && a.hidden != 64) return fail(NTBC_EFORMAT, "hidden %d not in {16,32,64}", a.hidden);
   if (a.n_hidden != 3) return fail(NTBC_EFORMAT, "n_hidden %d != 3 (PAPER.md:331)", a.n_hidden);
   if (a.F != 2) return fail(NTBC_EFORMAT, "features per level %d != 2 (PAPER.md:336)", a.F);
   int want_e = 0, want_c = 0;
   for (int i = 0; i < a.n_tex; i++) { want_e += a.fmt[i] == NTBC_BC1 ? 6 : 2; want_c += a.fmt[i] == NTBC_BC1 ? 3 : 1; }
+  if (a.naive) want_c = a.n_tex;   // one weight per texel per texture
   if (n_e != want_e || n_c != want_c) return fail(NTBC_EFORMAT, "head widths %d/%d inconsistent with formats", n_e, n_c);
   if (n_e > 48) return fail(NTBC_EFORMAT, "N_e = %d > 48 not supported", n_e);
   for (int g = 0; g < 2; g++) {
@@ -118,7 +122,7 @@ ntbc_status parse(const void* blob, size_t n, Arch& a) {
 }
 
 bool same_arch(const Arch& x, const Arch& y) {
-  if (x.n_tex != y.n_tex || x.hidden != y.hidden || x.total != y.total) return false;
+  if (x.n_tex != y.n_tex || x.hidden != y.hidden || x.total != y.total || x.naive != y.naive) return false;
   for (int i = 0; i < x.n_tex; i++) if (x.fmt[i] != y.fmt[i]) return false;
   for (int g = 0; g < 2; g++) if (x.levels[g] != y.levels[g] || x.coarsest[g] != y.coarsest[g]) return false;
   return true;
@@ -251,7 +255,7 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
   for (int k = 0; k < a.n_tex; k++) {
     p.fmt[k] = a.fmt[k];
     p.ep_off[k] = eo;
-    p.col_off[k] = co;
+    p.col_off[k] = a.naive ? k : co;
     eo += a.fmt[k] == NTBC_BC1 ? 6 : 2;
     co += a.fmt[k] == NTBC_BC1 ? 3 : 1;
   }
@@ -262,7 +266,9 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
   const int maxo = a.dims[0][4] > a.dims[1][4] ? a.dims[0][4] : a.dims[1][4];
   const uint32_t a_kmajor = 128u * a.hidden * 2u, a_stage = 128u * 4u * (uint32_t)((maxo + 1) & ~1);  // pairs
   p.a_bytes = (uint32_t)((std::max(a_kmajor, a_stage) + 127) & ~127u);
-  p.pal_bytes = (uint32_t)(a.n_tex * 128 * 4);   // BC word headers only (palettes rebuilt per texel)
+  p.pal_bytes = (uint32_t)(a.n_tex * 128 * 5);   // BC word headers + BC1 swap flags (palettes rebuilt per texel)
+  p.pal_bytes = (p.pal_bytes + 15) & ~15u;
+  p.naive = a.naive;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -53,6 +53,7 @@ struct FusedParams {
   unsigned long long* progress; // optional: per-chunk count of finished units (pipelined D2H, see ntbc_api.cu)
   int chunk_rows;               // block rows per progress chunk
   int* next_unit;               // optional: dynamic unit counter (zeroed before the launch)
+  int naive;                    // 1: the texel net outputs one weight per texture (naive approach)
 };
 
 // ---------------------------------------------------------------- a1-a2: coordinates + grid encode
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   uint8_t* A = wg_base;                                           // [128][H] K-major fp16 / fp32 staging
   float* stage = reinterpret_cast<float*>(A);                     // [ch][128] fp32 (after the last MMA)
   uint32_t* hdrs = reinterpret_cast<uint32_t*>(wg_base + p.a_bytes);  // [tex][128 blocks] BC word low bits
+  uint8_t* swp = reinterpret_cast<uint8_t*>(hdrs + p.n_tex * 128);   // [tex][128 blocks] BC1 endpoint swap (naive)
   uint64_t* bars = reinterpret_cast<uint64_t*>(ones + 4096 + kUnormBytes + NWG * (p.a_bytes + p.pal_bytes));
   uint64_t* bar_mma = bars + wg;                                  // this work group's MMA completion
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
@@ -312,7 +314,9 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           float ep[6];
 #pragma unroll
           for (int c = 0; c < 6; c++) ep[c] = stage[(eo + c) * 128 + r];
-          hdrs[k * 128 + r] = quant_bc1_hdr(ep);
+          bool swapped;
+          hdrs[k * 128 + r] = quant_bc1_hdr(ep, swapped);
+          swp[k * 128 + r] = swapped;
         } else {                    // E0 | E1 << 8 (R13)
           const float ep[2] = {stage[eo * 128 + r], stage[(eo + 1) * 128 + r]};
           hdrs[k * 128 + r] = quant_bc4_hdr(ep);
@@ -344,7 +348,21 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           const int co = p.col_off[k];
           const uint32_t hdr = hdrs[k * 128 + b];
           uint64_t word;
-          if (p.fmt[k] == kFmtBC1) {  // palette endpoints = UNORM expansion of the header (R12)
+          if (p.naive) {  // naive approach: nearest palette weight to the predicted weight
+            const float w = stage[co * 128 + r];
+            if (p.fmt[k] == kFmtBC1) {
+              const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
+              uint32_t n = naive_bc1_index(w);
+              if (swp[k * 128 + b]) n = 3u - n;                  // weights follow the predicted endpoint order
+              const uint32_t code = c0 == c1 ? 0u : (0x1320u >> (4 * n)) & 3u;   // linear n -> code [0,2,3,1]
+              word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
+            } else {
+              const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
+              const uint32_t n = naive_bc4_index(w, E0 > E1, unorm + 352);
+              const uint32_t map = E0 > E1 ? 0x17654320u : 0x71543206u;
+              word = (uint64_t)hdr | (pack_bc4_indices((map >> (4 * n)) & 7u, lane) << 16);
+            }
+          } else if (p.fmt[k] == kFmtBC1) {  // palette endpoints = UNORM expansion of the header (R12)
             const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
             const float e0[3] = {unorm[c0 >> 11], unorm[32 + ((c0 >> 5) & 63)], unorm[c0 & 31]};
             const float e1[3] = {unorm[c1 >> 11], unorm[32 + ((c1 >> 5) & 63)], unorm[c1 & 31]};

@@ -58,14 +58,15 @@ class ModelSpec:
     block_coarsest: int = 16
     texel_levels: int = 8
     texel_coarsest: int = 16
+    naive: bool = False            # weight network (one weight per texel per texture)
 
     @property
     def n_endpoint_out(self) -> int:   # PAPER.md:388  6 N_RGB + 2 N_SC
         return sum(6 if f == BC1 else 2 for f in self.fmts)
 
     @property
-    def n_color_out(self) -> int:      # PAPER.md:388  3 N_RGB + N_SC
-        return sum(3 if f == BC1 else 1 for f in self.fmts)
+    def n_color_out(self) -> int:      # PAPER.md:388  3 N_RGB + N_SC; naive: one weight per texture
+        return len(self.fmts) if self.naive else sum(3 if f == BC1 else 1 for f in self.fmts)
 
     @property
     def endpoint_in(self) -> int:
@@ -99,6 +100,11 @@ CONFIGS = {
             spec=lambda: ModelSpec([BC1, BC1, BC1, BC1, BC4, BC4, BC4, BC4])),
     6: dict(name="C3p-4k-paper-Tab1-2bc1+4bc4", width=4096, height=4096,
             spec=lambda: ModelSpec([BC1, BC1, BC4, BC4, BC4, BC4])),
+    7: dict(name="C3-4k-naive-weight-net-2bc1+3bc4", width=4096, height=4096,
+            spec=lambda: ModelSpec([BC1, BC1, BC4, BC4, BC4], naive=True)),
+    8: dict(name="C1-64px-naive-bc1+bc4-tiny", width=64, height=64,
+            spec=lambda: ModelSpec([BC1, BC4], hidden=16, block_levels=2, block_coarsest=8, texel_levels=2,
+                                   texel_coarsest=16, naive=True)),
 }
 
 
@@ -163,6 +169,7 @@ def serialize(m: Model) -> bytes:
     hdr += struct.pack("<III", sp.hidden, sp.n_hidden, sp.features)
     hdr += struct.pack("<IIII", sp.block_levels, sp.block_coarsest, sp.texel_levels, sp.texel_coarsest)
     hdr += struct.pack("<IIII", sp.endpoint_in, sp.n_endpoint_out, sp.color_in, sp.n_color_out)
+    hdr += struct.pack("<I", 1 if sp.naive else 0)   # variant: 0 NTBC (colour network), 1 naive (weights)
     hdr = hdr.ljust(HEADER_BYTES, b"\0")
     parts = [hdr]
 

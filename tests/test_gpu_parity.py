@@ -221,6 +221,18 @@ def test_conservative_pair_and_mismatch_rules(ntbc):
             assert np.array_equal(host[k].numpy().view(np.uint64), ref[k])
 
 
+def test_naive_c1_full_material(ntbc):
+    """Naive approach: weight network + nearest palette weight, full tiny
+    material: MLP outputs bit-exact and every BC word equal to the oracle."""
+    W, H, _ = synth.config_shape(8)
+    check_material(ntbc, 8, W, H, [(0, H // 4)])
+
+
+def test_naive_4k_sampled_rows(ntbc):
+    W, H, _ = synth.config_shape(7)
+    check_material(ntbc, 7, W, H, [(0, 1), (517, 518), (H // 4 - 1, H // 4)])
+
+
 def test_tab1_conservative_pair_4k_sampled_rows(ntbc):
     """The paper's conservative workload (tools/tab1.py) at full size: an all-BC1 model and an
     all-BC4 model of the paper architecture decoded in one call; sampled rows of all 6 textures."""

@@ -511,3 +511,84 @@ def test_psnr_uniform_error_closed_form():
         b = a + np.float32(eps)
         ref = 20 * math.log10(1 / float(np.float32(eps)))
         assert abs(oracle.psnr(a, b) - ref) < 1e-3
+
+
+# ---------------------------------------------------------------- naive approach
+def test_naive_weight_quantization_spec_examples():
+    """SPEC quantize_weight examples: 0.34 -> n=1 (nearest of {0, 1/3, 2/3, 1}); 0 -> 0; BC4 E0 > E1 with
+    w = 0.5 exactly between 3/7 and 4/7 -> the lower n (3)."""
+    assert oracle.quantize_weight(0.34, synth.BC1) == 1
+    assert oracle.quantize_weight(0.0, synth.BC1) == 0
+    assert oracle.quantize_weight(1.0, synth.BC1) == 3
+    assert oracle.quantize_weight(0.5, synth.BC4, True) == 3
+    # 6-value mode: the weights (n-1)/5 of entries 1..6; the constant entries 0 and 7 are never chosen
+    ws = np.linspace(0.0, 1.0, 2001)
+    ns = {oracle.quantize_weight(float(w), synth.BC4, False) for w in ws}
+    assert ns == {1, 2, 3, 4, 5, 6}
+    assert oracle.quantize_weight(0.0, synth.BC4, False) == 1 and oracle.quantize_weight(1.0, synth.BC4, False) == 6
+
+
+def test_naive_encoding_decodes_to_nearest_palette_colour_of_the_weighted_mix():
+    """Independent pin of the naive encoders (Eq.7/8): every palette entry lies on the segment
+    between the quantized endpoints and is ordered by its weight, so the decoded texel of a naive block
+    must be the palette colour nearest to the weighted mix (1-w) e0 + w e1 of the endpoints in the
+    PREDICTED order -- which also pins the BC1 index remap when the 4-colour rule swaps them.  Weights
+    are drawn away from the midpoints between palette weights, where fp32 rounding decides ties."""
+    rng = np.random.default_rng(7)
+    checked_swap = 0
+    for _ in range(300):
+        ep = rng.uniform(0, 1, 6).astype(np.float32)
+        c0, c1 = oracle.rgb565(ep[:3]), oracle.rgb565(ep[3:])
+        if c0 == c1:
+            continue
+        e0, e1 = oracle.expand565(c0), oracle.expand565(c1)   # quantized endpoints, predicted order
+        ws = rng.uniform(0, 1, 16).astype(np.float32)
+        mid = np.array([1 / 6, 1 / 2, 5 / 6])
+        ws = np.where(np.min(np.abs(ws[:, None] - mid[None, :]), axis=1) < 1e-3, 0.25, ws).astype(np.float32)
+        blk = oracle.encode_bc1_naive(ep, ws)
+        dec = oracle.decode_block(blk, synth.BC1).reshape(16, 3)
+        want = [(1 - w) * e0 + w * e1 for w in ws.astype(np.float64)]
+        pal = [(1 - t) * e0 + t * e1 for t in (0, 1 / 3, 2 / 3, 1)]
+        for i in range(16):
+            best = min(pal, key=lambda c: np.sum((c - want[i]) ** 2))
+            assert np.allclose(dec[i], best, atol=1e-6), (i, ws[i], c0 < c1)
+        checked_swap += c0 < c1
+    assert checked_swap > 50
+    for mode8 in (True, False):
+        for _ in range(200):
+            E = sorted(rng.choice(256, 2, replace=False))
+            E0, E1 = (E[1], E[0]) if mode8 else (E[0], E[1])
+            ep = np.array([E0 / 255, E1 / 255], np.float32)
+            ws = rng.uniform(0, 1, 16).astype(np.float32)
+            steps = np.arange(7) / 7 if mode8 else np.arange(5) / 5
+            mids = (steps + (1 / 14 if mode8 else 1 / 10))
+            ws = np.where(np.min(np.abs(ws[:, None] - mids[None, :]), axis=1) < 1e-3, 0.02, ws).astype(np.float32)
+            blk = oracle.encode_bc4_naive(ep, ws)
+            dec = oracle.decode_block(blk, synth.BC4)
+            e0, e1 = E0 / 255, E1 / 255
+            cand = [(1 - n / 7) * e0 + n / 7 * e1 for n in range(8)] if mode8 else \
+                   [(1 - n / 5) * e0 + n / 5 * e1 for n in range(6)]
+            for i in range(16):
+                want = (1 - float(ws[i])) * e0 + float(ws[i]) * e1
+                assert abs(dec[i] - min(cand, key=lambda c: abs(c - want))) < 1e-6
+
+
+def test_naive_model_container_and_material():
+    """The variant flag round-trips through the container; a naive model's texel net has one output
+    per texture and decode_material equals the naive encoders applied to mlp_outputs."""
+    for cfg in (7, 8):
+        m = oracle.Model(synth.model_blob(cfg))
+        assert m.naive and m.n_c == m.n_tex
+    m = oracle.Model(synth.model_blob(8))
+    W, H, _ = synth.config_shape(8)
+    words = m.decode_material(W, H)
+    ep, w = m.mlp_outputs(W, H)
+    eo = 0
+    for k, f in enumerate(m.fmts):
+        for by in (0, 7, H // 4 - 1):
+            for bx in (0, 5, W // 4 - 1):
+                ws = np.array([w[4 * by + i // 4, 4 * bx + i % 4, k] for i in range(16)], np.float32)
+                e = ep[by, bx, eo:eo + (6 if f == synth.BC1 else 2)]
+                enc = oracle.encode_bc1_naive(e, ws) if f == synth.BC1 else oracle.encode_bc4_naive(e, ws)
+                assert words[k, by, bx] == np.uint64(enc)
+        eo += 6 if f == synth.BC1 else 2

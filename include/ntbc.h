@@ -47,6 +47,8 @@ typedef struct {
   int n_endpoint_out;      /* N_e = 6 N_RGB + 2 N_SC */
   int n_color_out;         /* N_c = 3 N_RGB + N_SC */
   int block_levels, block_coarsest, texel_levels, texel_coarsest, features;
+  int variant;             /* 0: NTBC colour network; 1: naive weight network with
+                              n_color_out = n_textures weights per texel (DESIGN R21-R23) */
   size_t device_bytes;     /* device memory held by the model */
 } ntbc_model_info;
 

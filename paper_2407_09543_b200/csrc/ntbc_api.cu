@@ -439,6 +439,7 @@ ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out) {
   out->texel_levels = a.levels[1];
   out->texel_coarsest = a.coarsest[1];
   out->features = a.F;
+  out->variant = a.naive;
   out->device_bytes = m->blob_cap * (m->slot_blob[1] ? 2 : 1) + m->scratch_bytes;
   return NTBC_OK;
 }

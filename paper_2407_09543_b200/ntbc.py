@@ -29,7 +29,7 @@ class _Info(C.Structure):
     _fields_ = [("n_textures", C.c_int), ("fmt", C.c_int * 8), ("hidden", C.c_int), ("n_hidden", C.c_int),
                 ("n_endpoint_out", C.c_int), ("n_color_out", C.c_int), ("block_levels", C.c_int),
                 ("block_coarsest", C.c_int), ("texel_levels", C.c_int), ("texel_coarsest", C.c_int),
-                ("features", C.c_int), ("device_bytes", C.c_size_t)]
+                ("features", C.c_int), ("variant", C.c_int), ("device_bytes", C.c_size_t)]
 
 
 _SIGS = {
@@ -89,6 +89,7 @@ class Model:
         self.hidden = info.hidden
         self.n_e, self.n_c = info.n_endpoint_out, info.n_color_out
         self.device_bytes = info.device_bytes
+        self.naive = bool(info.variant)
 
     @property
     def handle(self):

@@ -205,11 +205,11 @@ struct DevGuard {
 
 template <int H, int NWG, bool DUMP>
 ntbc_status launch_fused_t(const FusedParams& p, size_t smem, int grid, cudaStream_t st) {
-  auto kern = fused_decode_kernel<H, NWG, DUMP>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
+  auto kern = p.naive ? fused_decode_kernel<H, NWG, DUMP, true> : fused_decode_kernel<H, NWG, DUMP, false>;
+  static bool configured[2] = {false, false};  // per instantiation
+  if (!configured[p.naive]) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
+    configured[p.naive] = true;
   }
   kern<<<grid, NWG * 128, smem, st>>>(p);
   g_launches++;

@@ -137,7 +137,7 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, in
 // (128 blocks) then up to 16 colour tiles (8 blocks = 128 texels).  More independent groups per SM
 // hide more of the dependent epilogue latency.  Units are claimed from a global
 // counter (dynamic scheduling) so they finish in row order (pipelined copy-back, ntbc_api.cu).
-template <int H, int NWG, bool DUMP>
+template <int H, int NWG, bool DUMP, bool NAIVE>
 __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5, lane = tid & 31;
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           for (int c = 0; c < 6; c++) ep[c] = stage[(eo + c) * 128 + r];
           bool swapped;
           hdrs[k * 128 + r] = quant_bc1_hdr(ep, swapped);
-          swp[k * 128 + r] = swapped;
+          if (NAIVE) swp[k * 128 + r] = swapped;
         } else {                    // E0 | E1 << 8 (R13)
           const float ep[2] = {stage[eo * 128 + r], stage[(eo + 1) * 128 + r]};
           hdrs[k * 128 + r] = quant_bc4_hdr(ep);
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           const int co = p.col_off[k];
           const uint32_t hdr = hdrs[k * 128 + b];
           uint64_t word;
-          if (p.naive) {  // naive approach: nearest palette weight to the predicted weight
+          if (NAIVE) {  // naive approach: nearest palette weight to the predicted weight
             const float w = stage[co * 128 + r];
             if (p.fmt[k] == kFmtBC1) {
               const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;

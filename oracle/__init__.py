@@ -63,6 +63,9 @@ def lib():
             "o_encode_bc1": (u64, [vp, vp]),
             "o_encode_bc4": (u64, [vp, vp]),
             "o_quantize_weight": (i32, [f32, i32, i32]),
+            "o_encode_ref_bc1": (u64, [vp, i32]),
+            "o_encode_ref_bc4": (u64, [vp, i32]),
+            "o_encode_ref_texture": (None, [vp, i32, i32, i32, i32, vp, i32]),
             "o_encode_bc1_naive": (u64, [vp, vp]),
             "o_encode_bc4_naive": (u64, [vp, vp]),
             "o_decode_block": (None, [u64, i32, vp]),
@@ -213,6 +216,23 @@ def rgb565(e3) -> int:
 def expand565(c: int) -> np.ndarray:
     out = np.zeros(3, np.float32)
     lib().o_expand565(int(c), _p(out))
+    return out
+
+
+def encode_ref_block(texels, fmt: int, n_refine: int = 2) -> int:
+    """Reference BC encoder of one 4x4 block (SPEC encode_block_reference; 16x3 for BC1, 16 for BC4)."""
+    t = np.ascontiguousarray(texels, np.float32).reshape(-1)
+    f = lib().o_encode_ref_bc1 if fmt == 1 else lib().o_encode_ref_bc4
+    return int(f(_p(t), int(n_refine)))
+
+
+def encode_ref_texture(tex, n_refine: int = 2, nthreads: int = 0) -> np.ndarray:
+    """fp32 [H][W][C] texture (C = 3 -> BC1, 1 -> BC4) -> uint64 [H/4][W/4] blocks."""
+    t = np.ascontiguousarray(tex, np.float32)
+    H, W = t.shape[:2]
+    C = t.shape[2] if t.ndim == 3 else 1
+    out = np.zeros((H // 4, W // 4), np.uint64)
+    lib().o_encode_ref_texture(_p(t), W, H, C, int(n_refine), _p(out), nthreads)
     return out
 
 

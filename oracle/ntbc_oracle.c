@@ -504,6 +504,177 @@ uint64_t o_encode_bc4_naive(const float ep[2], const float* w) {
     return blk;
 }
 
+/* ------------------------------------------------------------------------- */
+/* Reference BC1/BC4 encoder: the stand-in for Compressonator's "two refine steps"  */
+/* specified by SPEC encode_block_reference, in the op order of       */
+/* DESIGN.md R24-R29.  Texel values in [0,1]; fp32 with explicit fmaf, IEEE division.               */
+/* ------------------------------------------------------------------------- */
+static float clamp01(float x) { return fminf(fmaxf(x, 0.0f), 1.0f); }
+
+/* R26: 2x2 least squares for the endpoints of one channel set given per-texel weights w_i
+   (e0 has weight 0, e1 weight 1): A = sum (1-w)^2, B = sum w(1-w), D = sum w^2, P = sum (1-w)x,
+   Q = sum w x; e0 = (D P - B Q)/det, e1 = (A Q - B P)/det, det = A D - B^2.  Returns 0 (keep the
+   previous endpoints) when det is not positive. */
+static int ls_endpoints(int n, const float* w, const float* x, int nc, const int* use, float* e0, float* e1) {
+    float A = 0.0f, B = 0.0f, D = 0.0f, P[3] = {0, 0, 0}, Q[3] = {0, 0, 0};
+    for (int i = 0; i < n; i++) {
+        if (use && !use[i]) continue;
+        float wi = w[i], wb = 1.0f - wi;
+        A = fmaf(wb, wb, A); B = fmaf(wi, wb, B); D = fmaf(wi, wi, D);
+        for (int c = 0; c < nc; c++) { P[c] = fmaf(wb, x[i * nc + c], P[c]); Q[c] = fmaf(wi, x[i * nc + c], Q[c]); }
+    }
+    float det = fmaf(A, D, -(B * B));
+    if (!(det > 0.0f)) return 0;
+    for (int c = 0; c < nc; c++) {
+        e0[c] = clamp01(fmaf(D, P[c], -(B * Q[c])) / det);
+        e1[c] = clamp01(fmaf(A, Q[c], -(B * P[c])) / det);
+    }
+    return 1;
+}
+
+/* R24/R25: BC1 initial endpoints = extremes of the texels projected on the principal axis */
+static void bc1_pca_endpoints(const float* tx, float e0[3], float e1[3]) {
+    float mu[3] = {0, 0, 0};
+    for (int i = 0; i < 16; i++) for (int c = 0; c < 3; c++) mu[c] += tx[3 * i + c];
+    for (int c = 0; c < 3; c++) mu[c] *= 0.0625f;
+    float C[3][3] = {{0}};
+    for (int i = 0; i < 16; i++) {
+        float d[3] = {tx[3 * i] - mu[0], tx[3 * i + 1] - mu[1], tx[3 * i + 2] - mu[2]};
+        for (int a = 0; a < 3; a++) for (int b = a; b < 3; b++) C[a][b] = fmaf(d[a], d[b], C[a][b]);
+    }
+    C[1][0] = C[0][1]; C[2][0] = C[0][2]; C[2][1] = C[1][2];
+    /* start vector: the covariance column of the channel with the largest variance (first maximum);
+       never orthogonal to the principal axis of a line of texels (a fixed start like (1,1,1) is, e.g.
+       for a red-blue line) */
+    int k = 0;
+    for (int a = 1; a < 3; a++) if (C[a][a] > C[k][k]) k = a;
+    float v[3] = {C[0][k], C[1][k], C[2][k]};
+    int ok = C[k][k] > 0.0f;
+    for (int it = 0; it < 8 && ok; it++) {                     /* power iteration, max-abs normalised */
+        float u[3];
+        for (int a = 0; a < 3; a++) u[a] = fmaf(C[a][2], v[2], fmaf(C[a][1], v[1], C[a][0] * v[0]));
+        float m = fmaxf(fabsf(u[0]), fmaxf(fabsf(u[1]), fabsf(u[2])));
+        if (!(m > 0.0f)) { ok = 0; break; }
+        for (int a = 0; a < 3; a++) v[a] = u[a] / m;
+    }
+    if (!ok) {                                                 /* zero covariance: per-channel max / min */
+        for (int c = 0; c < 3; c++) { e0[c] = tx[c]; e1[c] = tx[c]; }
+        for (int i = 1; i < 16; i++) for (int c = 0; c < 3; c++) {
+            e0[c] = fmaxf(e0[c], tx[3 * i + c]); e1[c] = fminf(e1[c], tx[3 * i + c]);
+        }
+        return;
+    }
+    float tmin = 0.0f, tmax = 0.0f;
+    for (int i = 0; i < 16; i++) {
+        float t = fmaf(tx[3 * i + 2] - mu[2], v[2], fmaf(tx[3 * i + 1] - mu[1], v[1], (tx[3 * i] - mu[0]) * v[0]));
+        if (i == 0 || t < tmin) tmin = t;
+        if (i == 0 || t > tmax) tmax = t;
+    }
+    /* extremes along the axis: mu + (t / |v|^2) v (v is max-abs normalised, not unit length) */
+    float vv = fmaf(v[2], v[2], fmaf(v[1], v[1], v[0] * v[0]));
+    float smax = tmax / vv, smin = tmin / vv;
+    for (int c = 0; c < 3; c++) { e0[c] = clamp01(fmaf(smax, v[c], mu[c])); e1[c] = clamp01(fmaf(smin, v[c], mu[c])); }
+}
+
+/* final BC1 word for quantized endpoints (c0, c1) in either order: 4-colour order, per-texel argmin */
+static uint64_t bc1_word(uint16_t c0, uint16_t c1, const float* tx) {
+    if (c0 < c1) { uint16_t t = c0; c0 = c1; c1 = t; }
+    uint64_t w = (uint64_t)c0 | ((uint64_t)c1 << 16);
+    if (c0 == c1) return w;
+    float e0[3], e1[3], pal[4][3];
+    o_expand565(c0, e0); o_expand565(c1, e1);
+    o_palette_bc1(e0, e1, pal);
+    for (int i = 0; i < 16; i++) w |= (uint64_t)MAP1[o_argmin_bc1(tx + 3 * i, pal)] << (32 + 2 * i);
+    return w;
+}
+
+uint64_t o_encode_ref_bc1(const float* tx, int n_refine) {
+    float e0[3], e1[3];
+    bc1_pca_endpoints(tx, e0, e1);
+    uint16_t c0 = o_rgb565(e0), c1 = o_rgb565(e1);
+    for (int r = 0; r < n_refine && c0 != c1; r++) {           /* R26: least squares on the assignment */
+        float q0[3], q1[3], pal[4][3], w[16];
+        o_expand565(c0, q0); o_expand565(c1, q1);
+        o_palette_bc1(q0, q1, pal);
+        for (int i = 0; i < 16; i++) w[i] = (float)o_argmin_bc1(tx + 3 * i, pal) / 3.0f;
+        float n0[3], n1[3];
+        if (!ls_endpoints(16, w, tx, 3, NULL, n0, n1)) break;
+        c0 = o_rgb565(n0); c1 = o_rgb565(n1);
+    }
+    return bc1_word(c0, c1, tx);
+}
+
+/* BC4 candidate of one mode: squared error of the final assignment, word via o_encode_bc4's rules */
+static float bc4_err(uint8_t E0, uint8_t E1, const float* tx, int* n_out) {
+    float pal[8], err = 0.0f;
+    o_palette_bc4(E0, E1, pal);
+    for (int i = 0; i < 16; i++) {
+        int n = o_argmin_bc4(tx[i], pal);
+        if (n_out) n_out[i] = n;
+        float d = tx[i] - pal[n];
+        err = fmaf(d, d, err);
+    }
+    return err;
+}
+/* R27: enforce the candidate's mode on quantized endpoints (mode 8: E0 > E1, mode 6: E0 <= E1) */
+static void bc4_order(int mode8, uint8_t* E0, uint8_t* E1) {
+    if (mode8) {
+        if (*E0 < *E1) { uint8_t t = *E0; *E0 = *E1; *E1 = t; }
+        if (*E0 == *E1) { if (*E0 < 255) (*E0)++; else (*E1)--; }
+    } else if (*E0 > *E1) { uint8_t t = *E0; *E0 = *E1; *E1 = t; }
+}
+
+static float bc4_candidate(int mode8, const float* tx, int n_refine, uint8_t* oE0, uint8_t* oE1) {
+    float lo = 2.0f, hi = -1.0f;                              /* R28: min/max (mode 6: without exact 0 and 1) */
+    for (int i = 0; i < 16; i++) {
+        if (!mode8 && (tx[i] == 0.0f || tx[i] == 1.0f)) continue;
+        lo = fminf(lo, tx[i]); hi = fmaxf(hi, tx[i]);
+    }
+    if (hi < lo) { lo = 0.0f; hi = 1.0f; }                    /* mode 6 with only 0/1 texels */
+    uint8_t E0 = mode8 ? o_unorm8(hi) : o_unorm8(lo), E1 = mode8 ? o_unorm8(lo) : o_unorm8(hi);
+    bc4_order(mode8, &E0, &E1);
+    for (int r = 0; r < n_refine; r++) {
+        int n[16], use[16];
+        float w[16];
+        bc4_err(E0, E1, tx, n);
+        for (int i = 0; i < 16; i++) {
+            use[i] = mode8 || (n[i] >= 1 && n[i] <= 6);         /* the constants 0 and 1 carry no weight */
+            w[i] = mode8 ? (float)n[i] / 7.0f : (float)(n[i] - 1) / 5.0f;
+        }
+        float e0, e1;
+        if (!ls_endpoints(16, w, tx, 1, use, &e0, &e1)) break;
+        E0 = o_unorm8(e0); E1 = o_unorm8(e1);
+        bc4_order(mode8, &E0, &E1);
+    }
+    *oE0 = E0; *oE1 = E1;
+    return bc4_err(E0, E1, tx, NULL);
+}
+
+uint64_t o_encode_ref_bc4(const float* tx, int n_refine) {
+    uint8_t a0, a1, b0, b1;
+    float ea = bc4_candidate(1, tx, n_refine, &a0, &a1), eb = bc4_candidate(0, tx, n_refine, &b0, &b1);
+    float ep[2];
+    if (eb < ea) { a0 = b0; a1 = b1; }                        /* R29: lower error, ties -> 8-value mode */
+    ep[0] = (float)a0 / 255.0f; ep[1] = (float)a1 / 255.0f;   /* re-quantizes to exactly (a0, a1) */
+    return o_encode_bc4(ep, tx);
+}
+
+/* whole texture: row-major blocks; tex = fp32 [H][W][C] (C = 3 -> BC1, 1 -> BC4) */
+void o_encode_ref_texture(const float* tex, int W, int H, int C, int n_refine, uint64_t* out, int nthreads) {
+    int BW = W / 4, BH = H / 4;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int by = 0; by < BH; by++)
+        for (int bx = 0; bx < BW; bx++) {
+            float tx[48];
+            for (int i = 0; i < 16; i++)
+                for (int c = 0; c < C; c++) tx[i * C + c] = tex[((size_t)(4 * by + (i >> 2)) * W + 4 * bx + (i & 3)) * C + c];
+            out[(size_t)by * BW + bx] = C == 3 ? o_encode_ref_bc1(tx, n_refine) : o_encode_ref_bc4(tx, n_refine);
+        }
+}
+
 void o_decode_block(uint64_t blk, int fmt, float* out) {
     if (fmt == BC1) {
         uint16_t c0 = (uint16_t)blk, c1 = (uint16_t)(blk >> 16);

@@ -75,6 +75,12 @@ int      o_argmin_bc1(const float c[3], float pal[4][3]);      /* Eq.9-10 */
 int      o_argmin_bc4(float c, const float pal[8]);            /* Eq.9-10 */
 uint64_t o_encode_bc1(const float ep[6], const float* texels /* 16 x 3 */);
 uint64_t o_encode_bc4(const float ep[2], const float* texels /* 16 */);
+/* reference encoder (SPEC encode_block_reference, DESIGN R24-R29): PCA / min-max endpoints,
+   n_refine least-squares refinements (2 = the paper's Compressonator setting) */
+uint64_t o_encode_ref_bc1(const float* texels /* 16 x 3 */, int n_refine);
+uint64_t o_encode_ref_bc4(const float* texels /* 16 */, int n_refine);
+void     o_encode_ref_texture(const float* tex /* [H][W][C] */, int W, int H, int C, int n_refine,
+                              uint64_t* out /* [H/4][W/4] */, int nthreads);
 /* naive approach: nearest palette weight (ties -> lower n), linear index */
 int      o_quantize_weight(float w, int fmt, int mode8);
 uint64_t o_encode_bc1_naive(const float ep[6], const float* weights /* 16 */);

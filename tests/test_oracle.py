@@ -592,3 +592,78 @@ def test_naive_model_container_and_material():
                 enc = oracle.encode_bc1_naive(e, ws) if f == synth.BC1 else oracle.encode_bc4_naive(e, ws)
                 assert words[k, by, bx] == np.uint64(enc)
         eo += 6 if f == synth.BC1 else 2
+
+
+# ---------------------------------------------------------------- reference encoder
+def _codes(blk, fmt):
+    return [(blk >> (32 + 2 * i)) & 3 for i in range(16)] if fmt == synth.BC1 else \
+           [(blk >> (16 + 3 * i)) & 7 for i in range(16)]
+
+
+def _with_code(blk, fmt, i, code):
+    sh, m = (32 + 2 * i, 3) if fmt == synth.BC1 else (16 + 3 * i, 7)
+    return (blk & ~(m << sh)) | (code << sh)
+
+
+def test_ref_encoder_spec_examples():
+    # constant BC4 block at 0.5: decoded error per texel <= 1/510 (quantization bound)
+    blk = oracle.encode_ref_block(np.full(16, 0.5, np.float32), synth.BC4)
+    assert np.all(np.abs(oracle.decode_block(blk, synth.BC4) - 0.5) <= 1 / 510 + 1e-7)
+    # a block with exact 0 and 1 texels: the 6-value mode (E0 <= E1) represents both exactly and wins
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        t = rng.uniform(0.3, 0.7, 16).astype(np.float32)
+        t[rng.choice(16, 2, replace=False)] = [0.0, 1.0]
+        blk = oracle.encode_ref_block(t, synth.BC4)
+        assert (blk & 0xFF) <= ((blk >> 8) & 0xFF)
+        dec = oracle.decode_block(blk, synth.BC4)
+        assert np.all(dec[t == 0.0] == 0.0) and np.all(dec[t == 1.0] == 1.0)
+    # degenerate BC1 block (all texels one colour): c0 == c1, all codes 0, within half a 565 step
+    c = np.array([0.3, 0.6, 0.9], np.float32)
+    blk = oracle.encode_ref_block(np.tile(c, (16, 1)), synth.BC1)
+    assert (blk & 0xFFFF) == ((blk >> 16) & 0xFFFF) and (blk >> 32) == 0
+    assert np.all(np.abs(oracle.decode_block(blk, synth.BC1).reshape(16, 3) - c) <= np.array([1 / 62, 1 / 126, 1 / 62]))
+
+
+def test_ref_encoder_reproduces_a_representable_block_exactly():
+    """Texels drawn from the palette of two 565-representable endpoints lie on a line: the PCA axis,
+    its extremes, the assignment and the refinement must reproduce them with zero error (pins R24-R26)."""
+    rng = np.random.default_rng(11)
+    for c0, c1 in ((0xF800, 0x001F), (0x7BEF, 0x0000), (0xFFFF, 0x8410), (0x4A69, 0x2104)):
+        e0, e1 = oracle.expand565(c0), oracle.expand565(c1)
+        pal = oracle.palette_bc1(e0, e1)
+        for _ in range(20):
+            n = rng.integers(0, 4, 16)
+            n[:2] = [0, 3]                                   # both extremes present
+            tx = pal[n].astype(np.float32)
+            blk = oracle.encode_ref_block(tx, synth.BC1)
+            assert np.array_equal(oracle.decode_block(blk, synth.BC1).reshape(16, 3), tx), (hex(c0), hex(c1))
+
+
+def test_ref_encoder_index_optimality_and_bc1_mode_safety():
+    rng = np.random.default_rng(5)
+    for fmt, ch in ((synth.BC1, 3), (synth.BC4, 1)):
+        for _ in range(200):
+            tx = rng.uniform(0, 1, (16, ch)).astype(np.float32).reshape(-1)
+            blk = oracle.encode_ref_block(tx, fmt)
+            if fmt == synth.BC1:
+                c0, c1 = blk & 0xFFFF, (blk >> 16) & 0xFFFF
+                assert c0 > c1 or (c0 == c1 and (blk >> 32) == 0)
+            base = oracle.block_sq_error(blk, fmt, tx)
+            ncode = 4 if fmt == synth.BC1 else 8
+            for i in range(16):                               # no single index change lowers the error
+                for code in range(ncode):
+                    assert oracle.block_sq_error(_with_code(blk, fmt, i, code), fmt, tx) >= base - 1e-12
+            if fmt == synth.BC4:                              # and never beats the brute-force optimum
+                _, best = oracle.bruteforce_bc4(tx)
+                assert base >= best - 1e-12
+
+
+def test_ref_encoder_refinement_never_loses_psnr_on_noise():
+    """SPEC ablation oracle: two least-squares refinements beat the unrefined (projection-only)
+    endpoints on random noise, for both formats."""
+    rng = np.random.default_rng(9)
+    for ch, fmt in ((3, synth.BC1), (1, synth.BC4)):
+        tex = rng.uniform(0, 1, (32, 32, ch)).astype(np.float32)
+        p = {r: oracle.psnr(oracle.decode_bc(oracle.encode_ref_texture(tex, r), fmt, 32, 32), tex) for r in (0, 2)}
+        assert p[2] >= p[0], p

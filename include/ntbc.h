@@ -102,6 +102,17 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
                                       const size_t* blob_sizes, int width, int height,
                                       void* const* host_out, void* stream);
 
+/* reference BC1/BC4 encoder -- the documented stand-in for the paper's Compressonator
+ * "two refine steps" (SPEC encode_block_reference S:153-161; R24-R29):
+ * PCA (BC1) or min/max (BC4, both modes) endpoints, n_refine least-squares refinements of the
+ * endpoints on the current index assignment, BC1 4-colour order, BC4 lower-error mode, per-texel
+ * optimal indices on the final palette.  One thread per block.
+ *   texels: device, height*width*(3 for BC1 | 1 for BC4) fp32 in [0,1], row-major, RGB interleaved;
+ *   out_blocks: device, (height/4)*(width/4) u64 words, row-major, 8-B aligned; n_refine in [0, 8].
+ * Errors: NTBC_EINVAL, NTBC_ECUDA. */
+ntbc_status ntbc_encode_bc(const float* texels, ntbc_format fmt, int width, int height, int n_refine,
+                           void* out_blocks, void* stream);
+
 /* Row a9 (verification): decode a BC1/BC4 surface with the DirectX palettes (decode uses
  * the same float palette arithmetic as the encoder, R18) into fp32 texels.
  *   blocks: device, (height/4)*(width/4) words; out_texels: device, height*width*(3|1) fp32,

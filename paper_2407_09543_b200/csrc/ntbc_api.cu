@@ -13,6 +13,7 @@
 
 #include "../../include/ntbc.h"
 #include "ntbc_kernels.cuh"
+#include "refenc.cuh"
 
 using namespace ntbc;
 
@@ -593,6 +594,28 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
     }
     t += n_tex;
   }
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_encode_bc(const float* texels, ntbc_format fmt, int width, int height, int n_refine,
+                           void* out_blocks, void* stream) {
+  if (!texels || !out_blocks) return fail(NTBC_EINVAL, "NULL argument");
+  if (fmt != NTBC_BC1 && fmt != NTBC_BC4) return fail(NTBC_EINVAL, "bad format %d", (int)fmt);
+  if (n_refine < 0 || n_refine > 8) return fail(NTBC_EINVAL, "n_refine %d not in [0,8]", n_refine);
+  if ((uintptr_t)out_blocks & 7) return fail(NTBC_EINVAL, "out_blocks not 8-B aligned");
+  ntbc_status st = check_dims(width, height, 0, height / 4);
+  if (st) return st;
+  const long long nb = (long long)(width / 4) * (height / 4);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<long long>((nb + 127) / 128, (long long)sms * 16);
+  if (fmt == NTBC_BC1)
+    refenc_kernel<3><<<grid, 128, 0, (cudaStream_t)stream>>>(texels, width, height, n_refine, (uint64_t*)out_blocks);
+  else
+    refenc_kernel<1><<<grid, 128, 0, (cudaStream_t)stream>>>(texels, width, height, n_refine, (uint64_t*)out_blocks);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
   return NTBC_OK;
 }
 

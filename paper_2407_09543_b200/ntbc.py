@@ -40,6 +40,7 @@ _SIGS = {
     "ntbc_decode_material": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "ntbc_decode_material_host": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _vp]),
     "ntbc_decode_bc": (_i, [_vp, _i, _i, _i, _vp, _vp]),
+    "ntbc_encode_bc": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
     "ntbc_debug_mlp": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ntbc_debug_features": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ntbc_pack": (_i, [_i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
@@ -141,6 +142,14 @@ def decode_material_host(models, pinned_blobs, width: int, height: int, host_out
     outs = (_vp * len(host_outs))(*[o.data_ptr() for o in host_outs])
     _check(_lib.ntbc_decode_material_host(_handles(models), len(models), blobs, sizes, width, height, outs,
                                           _stream(stream)))
+
+
+def encode_bc(texels: torch.Tensor, fmt: int, width: int, height: int, n_refine: int = 2, out=None, stream=None):
+    """ntbc_encode_bc: reference BC1/BC4 encoder (fp32 [H][W][3|1] device texels -> int64 [H/4][W/4])."""
+    if out is None:
+        out = torch.empty((height // 4, width // 4), dtype=torch.int64, device=texels.device)
+    _check(_lib.ntbc_encode_bc(texels.data_ptr(), fmt, width, height, n_refine, out.data_ptr(), _stream(stream)))
+    return out
 
 
 def decode_bc(blocks: torch.Tensor, fmt: int, width: int, height: int, out=None, stream=None):

@@ -233,6 +233,36 @@ def test_naive_4k_sampled_rows(ntbc):
     check_material(ntbc, 7, W, H, [(0, 1), (517, 518), (H // 4 - 1, H // 4)])
 
 
+@pytest.mark.parametrize("fmt,ch", [(1, 3), (4, 1)])
+@pytest.mark.parametrize("n_refine", [0, 2])
+def test_reference_encoder_bit_exact(ntbc, fmt, ch, n_refine):
+    """the GPU reference encoder (ntbc_encode_bc) against the oracle's, every word, on a
+    smooth synthetic texture, uniform noise with exact 0/1 texels and constant regions (ragged size)."""
+    rng = np.random.default_rng(fmt * 10 + n_refine)
+    texs = [synth.texture(256, 128, ch, seed=fmt + n_refine)]
+    noise = rng.uniform(0, 1, (132, 260, ch)).astype(np.float32)
+    noise[::7, ::5] = 0.0
+    noise[3::11, 2::3] = 1.0
+    noise[:16, :16] = 0.25                                   # constant blocks (degenerate BC1, BC4 both modes)
+    texs.append(noise)
+    for tex in texs:
+        H, W = tex.shape[:2]
+        g = ntbc.encode_bc(torch.from_numpy(np.ascontiguousarray(tex)).to(DEV), fmt, W, H, n_refine)
+        o = oracle.encode_ref_texture(tex, n_refine)
+        assert np.array_equal(u64(g), o)
+
+
+def test_reference_encoder_4k_sampled_rows(ntbc):
+    W = H = 4096
+    rng = np.random.default_rng(1)
+    for fmt, ch in ((1, 3), (4, 1)):
+        tex = rng.uniform(0, 1, (H, W, ch)).astype(np.float32)
+        g = u64(ntbc.encode_bc(torch.from_numpy(tex).to(DEV), fmt, W, H))
+        for by in (0, 517, H // 4 - 1):
+            o = oracle.encode_ref_texture(tex[4 * by:4 * by + 4], 2)
+            assert np.array_equal(g[by:by + 1], o)
+
+
 def test_tab1_conservative_pair_4k_sampled_rows(ntbc):
     """The paper's conservative workload (tools/tab1.py) at full size: an all-BC1 model and an
     all-BC4 model of the paper architecture decoded in one call; sampled rows of all 6 textures."""

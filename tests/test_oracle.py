@@ -667,3 +667,28 @@ def test_ref_encoder_refinement_never_loses_psnr_on_noise():
         tex = rng.uniform(0, 1, (32, 32, ch)).astype(np.float32)
         p = {r: oracle.psnr(oracle.decode_bc(oracle.encode_ref_texture(tex, r), fmt, 32, 32), tex) for r in (0, 2)}
         assert p[2] >= p[0], p
+
+
+def test_dds_container_round_trip_and_pillow():
+    """SPEC dds_write/dds_read: 4x4 BC1 surface -> 128 + 8 bytes; read(write(s)) == s; Pillow's
+    independent DDS reader decodes our container like the oracle's decoder (within its +-2 LSB)."""
+    from PIL import Image
+    from paper_2407_09543_b200 import dds
+    blk = np.array([[0x55555555F800001F]], np.uint64)
+    assert len(dds.dds_bytes(blk, 1, 4, 4)) == 136
+    rng = np.random.default_rng(4)
+    for fmt, ch in ((1, 3), (4, 1)):
+        tex = rng.uniform(0, 1, (16, 24, ch)).astype(np.float32)
+        blocks = oracle.encode_ref_texture(tex)
+        data = dds.dds_bytes(blocks, fmt, 24, 16)
+        b2, f2, w2, h2 = dds.read_dds(data)
+        assert (f2, w2, h2) == (fmt, 24, 16) and np.array_equal(b2, blocks)
+        assert dds.dds_bytes(b2, f2, w2, h2) == data
+        img = Image.open(io.BytesIO(data))
+        img.load()
+        pil = np.asarray(img).astype(np.float64)
+        pil = pil[..., :3] if fmt == 1 else pil.reshape(16, 24, -1)[..., :1]
+        ours = oracle.decode_bc(blocks, fmt, 24, 16).astype(np.float64).reshape(16, 24, ch) * 255
+        assert np.max(np.abs(pil - ours)) <= 2.0 + 1e-9
+    with pytest.raises(ValueError):
+        dds.read_dds(b"XXXX" + data[4:])

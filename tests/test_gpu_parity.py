@@ -263,6 +263,29 @@ def test_reference_encoder_4k_sampled_rows(ntbc):
             assert np.array_equal(g[by:by + 1], o)
 
 
+@pytest.mark.parametrize("fmts,hidden,naive", [([synth.BC4] * 8, 32, False), ([synth.BC1] * 8, 64, False),
+                                               ([synth.BC1, synth.BC4] * 4, 64, True), ([synth.BC1] * 3, 16, True)])
+def test_extreme_head_layouts(ntbc, fmts, hidden, naive):
+    """Eight textures of one format (widest endpoint head N_e = 48, all-BC4 colour head), hidden 16/32,
+    naive variants; a ragged 1k-wide material (units that end mid-row), full rows compared."""
+    sp = synth.ModelSpec(list(fmts), hidden=hidden, naive=naive)
+    blob = synth.serialize(synth.random_model(sp, len(fmts) * 100 + hidden))
+    check_material(ntbc, blob, 4 * 300, 4 * 6, [(0, 6)])
+
+
+def test_host_entry_point_naive_model(ntbc):
+    W, H, _ = synth.config_shape(8)
+    blob = synth.model_blob(8, material=2)
+    m = ntbc.Model(synth.model_blob(8))
+    pinned = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
+    host = [torch.full((H // 4, W // 4), -1, dtype=torch.int64).pin_memory() for _ in range(m.n_tex)]
+    ntbc.decode_material_host([m], [pinned], W, H, host)
+    torch.cuda.synchronize()
+    ref = oracle.Model(blob).decode_material(W, H)
+    for k in range(m.n_tex):
+        assert np.array_equal(host[k].numpy().view(np.uint64), ref[k])
+
+
 def test_tab1_conservative_pair_4k_sampled_rows(ntbc):
     """The paper's conservative workload (tools/tab1.py) at full size: an all-BC1 model and an
     all-BC4 model of the paper architecture decoded in one call; sampled rows of all 6 textures."""

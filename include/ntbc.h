@@ -113,6 +113,27 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
 ntbc_status ntbc_encode_bc(const float* texels, ntbc_format fmt, int width, int height, int n_refine,
                            void* out_blocks, void* stream);
 
+/* one training step of the colour network (Eq. 14-15 / P:285-304 / App. A,
+ * Adam P:340-341; R30-R32).  fp32 parameters in one flat device vector, layout: the texel
+ * grid levels coarse -> fine, each [res][res][2] (res = coarsest << l), then per layer l = 0..3
+ * W_l [in][out] and b_l [out] of the 2*levels -> hidden x3 -> N_c colour MLP.  The step zeroes `grads`,
+ * computes loss = mean over the batch of sum over textures (|c_hat - c|^2 + |c_dec - c|^2) with the
+ * STE expectation at temperature T for the argmax, accumulates its gradient, and applies one
+ * bias-corrected Adam update (beta1 0.9, beta2 0.999, eps 1e-15; lr_grid for the grid entries, lr_mlp
+ * for the MLP) with step number `step` (>= 1).
+ *   xy: device int32 [B][2] texel coordinates (< W, H); cref: device fp32 [B][N_c] reference colours
+ *   (head order); eref: device fp32 [B][N_e] reference endpoints of each texel's block (BC1: e0 rgb,
+ *   e1 rgb; BC4: e0, e1); loss: device fp32 scalar (overwritten).  Not deterministic in the last bits
+ *   (atomic accumulation order).  Errors: NTBC_EINVAL, NTBC_ECUDA. */
+typedef struct {
+  int n_textures, fmt[8], hidden, levels, coarsest;
+} ntbc_train_arch;
+long long ntbc_train_param_count(const ntbc_train_arch* arch);   /* floats in the parameter vector; <0: invalid */
+ntbc_status ntbc_train_colour_step(const ntbc_train_arch* arch, float* params, float* grads, float* adam_m,
+                                   float* adam_v, int step, const int* xy, const float* cref, const float* eref,
+                                   int batch, int width, int height, float temperature, float lr_grid,
+                                   float lr_mlp, float* loss, void* stream);
+
 /* Row a9 (verification): decode a BC1/BC4 surface with the DirectX palettes (decode uses
  * the same float palette arithmetic as the encoder, R18) into fp32 texels.
  *   blocks: device, (height/4)*(width/4) words; out_texels: device, height*width*(3|1) fp32,

@@ -1,0 +1,134 @@
+"""Training-step ORACLE for the NTBC colour network -- TEST INFRASTRUCTURE ONLY.
+
+Plain PyTorch float64 on the CPU, autograd for the backward pass; only tests/ and bench-side tools
+may import it.  Shares no code with the CUDA path.  One step follows PAPER.md:
+
+  * features: the texel grid (fp32 master values, [res][res][2] per level, levels coarse -> fine) sampled
+    at the texel centre exactly as at inference (R1-R3; no QAT: the 90% float phase);
+  * colour MLP 16 -> H -> H -> H -> N_c, selu hidden, sigmoid out, fp32 master weights;
+  * loss L_color = L_c + L_cd (Eq. 14-15), per texel and texture:
+      L_c  = |c_hat - c|^2,
+      L_cd = |c_dec - c|^2 with c_dec the palette colour of the reference endpoints (Eq. 7/8) at
+             n = argmax_n d_n, d_n = -|c_hat - c_n| (Eq. 9-10, colour-network case);
+    averaged over the batch (R30);
+  * STE through the argmax (App. A): forward uses c_dec, backward differentiates the
+    expectation sum_n softmax(d/T)_n c_n (for BC1 this is (1 - w_hat) e0 + w_hat e1 with the expected
+    weight w_hat of Eq. expected_weight; its derivative is (1/T) sigma_n (w_n - w_hat) -- App. A's
+    Eq. devExtW prints "n - w_hat", a typo for w_n - w_hat); T = 0.01;
+  * Adam, beta1 = 0.9, beta2 = 0.999, eps = 1e-15, separate learning rates for grids and MLP
+    (P:341), bias-corrected as in Kingma & Ba.
+
+Parameter vector layout (shared with the C ABI, R30): grid levels in order, each
+[res][res][2] y-major; then per layer W [in][out] and b [out].
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+BC1, BC4 = 1, 4
+
+
+def layout(fmts, hidden, levels, coarsest):
+    """[(name, shape)] of the flat parameter vector."""
+    n_c = sum(3 if f == BC1 else 1 for f in fmts)
+    out = [(f"grid{l}", (coarsest << l, coarsest << l, 2)) for l in range(levels)]
+    dims = [2 * levels, hidden, hidden, hidden, n_c]
+    for l in range(4):
+        out += [(f"W{l}", (dims[l], dims[l + 1])), (f"b{l}", (dims[l + 1],))]
+    return out
+
+
+def unflatten(vec, lay):
+    parts, off = {}, 0
+    for name, shape in lay:
+        n = int(np.prod(shape))
+        parts[name] = vec[off:off + n].reshape(shape)
+        off += n
+    return parts
+
+
+def grid_features(grids, u, v):
+    """Vertex-centred bilinear lookup per level (R1), concatenated coarse -> fine (R3)."""
+    feats = []
+    for g in grids:
+        res = g.shape[0]
+        X, Y = u * (res - 1), v * (res - 1)
+        i0 = torch.clamp(torch.floor(X), max=res - 2).long()
+        j0 = torch.clamp(torch.floor(Y), max=res - 2).long()
+        fx, fy = (X - i0)[:, None], (Y - j0)[:, None]
+        v00, v10 = g[j0, i0], g[j0, i0 + 1]
+        v01, v11 = g[j0 + 1, i0], g[j0 + 1, i0 + 1]
+        top = v00 + fx * (v10 - v00)
+        bot = v01 + fx * (v11 - v01)
+        feats.append(top + fy * (bot - top))
+    return torch.cat(feats, dim=1)
+
+
+def palettes(fmt, eref):
+    """Palette colours [B][n][ch] of the reference endpoints (Eq. 7 / Eq. 8)."""
+    if fmt == BC1:
+        e0, e1 = eref[:, None, 0:3], eref[:, None, 3:6]
+        w = torch.arange(4, dtype=eref.dtype)[None, :, None] / 3
+        return (1 - w) * e0 + w * e1
+    e0, e1 = eref[:, 0:1], eref[:, 1:2]
+    m8 = (e0 > e1)
+    w8 = torch.arange(8, dtype=eref.dtype)[None, :] / 7
+    pal8 = (1 - w8) * e0 + w8 * e1
+    w6 = (torch.arange(8, dtype=eref.dtype)[None, :] - 1) / 5
+    pal6 = (1 - w6) * e0 + w6 * e1
+    pal6 = torch.cat([torch.zeros_like(e0), pal6[:, 1:7], torch.ones_like(e0)], dim=1)
+    return torch.where(m8, pal8, pal6)[:, :, None]
+
+
+def ste_decoded(chat, pal, T):
+    """c_dec in the forward pass, d(sum softmax(d/T) c_n) in the backward pass (App. A)."""
+    diff = chat[:, None, :] - pal
+    dist = torch.sqrt(torch.clamp((diff * diff).sum(-1), min=1e-30))   # |c_hat - c_n| (gradient-safe at 0)
+    d = -dist
+    n = torch.argmax(d, dim=1)                                          # first maximum: ties -> lower n
+    hard = pal[torch.arange(pal.shape[0]), n]
+    soft = (torch.softmax(d / T, dim=1)[:, :, None] * pal).sum(1)
+    return soft + (hard - soft).detach()
+
+
+def colour_loss(params, lay, fmts, xy, W, H, cref, eref, T):
+    p = unflatten(params, lay)
+    levels = sum(1 for name, _ in lay if name.startswith("grid"))
+    u = (xy[:, 0].double() + 0.5) / W
+    v = (xy[:, 1].double() + 0.5) / H
+    a = grid_features([p[f"grid{l}"] for l in range(levels)], u, v)
+    for l in range(3):
+        a = torch.nn.functional.selu(a @ p[f"W{l}"] + p[f"b{l}"])
+    chat = torch.sigmoid(a @ p["W3"] + p["b3"])
+    loss = torch.zeros((), dtype=torch.float64)
+    co = eo = 0
+    for f in fmts:
+        w, we = (3, 6) if f == BC1 else (1, 2)
+        c, ch = cref[:, co:co + w], chat[:, co:co + w]
+        dec = ste_decoded(ch, palettes(f, eref[:, eo:eo + we]), T)
+        loss = loss + ((ch - c) ** 2).sum() + ((dec - c) ** 2).sum()
+        co += w
+        eo += we
+    return loss / xy.shape[0]
+
+
+def adam(params, grads, m, v, step, lr, beta1=0.9, beta2=0.999, eps=1e-15):
+    """One bias-corrected Adam update (Kingma & Ba): returns (params, m, v)."""
+    m = beta1 * m + (1 - beta1) * grads
+    v = beta2 * v + (1 - beta2) * grads * grads
+    mh = m / (1 - beta1 ** step)
+    vh = v / (1 - beta2 ** step)
+    return params - lr * mh / (torch.sqrt(vh) + eps), m, v
+
+
+def colour_step(params, m, v, step, lay, fmts, xy, W, H, cref, eref, T=0.01, lr_grid=0.01, lr_mlp=0.005):
+    """One training step; all arrays float64 torch tensors (xy int).  Returns (loss, grads, params, m, v)."""
+    x = params.clone().requires_grad_(True)
+    loss = colour_loss(x, lay, fmts, xy, W, H, cref, eref, T)
+    (g,) = torch.autograd.grad(loss, x)
+    n_grid = sum(int(np.prod(s)) for name, s in lay if name.startswith("grid"))
+    lr = torch.full_like(params, lr_mlp)
+    lr[:n_grid] = lr_grid
+    p2, m2, v2 = adam(params, g, m, v, step, lr)
+    return float(loss.detach()), g, p2, m2, v2

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -14,6 +15,7 @@
 #include "../../include/ntbc.h"
 #include "ntbc_kernels.cuh"
 #include "refenc.cuh"
+#include "train.cuh"
 
 using namespace ntbc;
 
@@ -135,6 +137,7 @@ int round16(int v) { return (v + 15) & ~15; }
 
 constexpr int kMaxChunks = 64;
 constexpr int kSchedRing = 64;
+thread_local long long g_train_total = 0;   // parameter count of the last train_layout
 // chunk c is copied on copy stream c % kCopyStreams: each stream-wait operation has a fixed latency,
 // so consecutive chunks' waits must not queue behind each other on one stream
 constexpr int kCopyStreams = 4;
@@ -614,6 +617,82 @@ ntbc_status ntbc_encode_bc(const float* texels, ntbc_format fmt, int width, int 
     refenc_kernel<3><<<grid, 128, 0, (cudaStream_t)stream>>>(texels, width, height, n_refine, (uint64_t*)out_blocks);
   else
     refenc_kernel<1><<<grid, 128, 0, (cudaStream_t)stream>>>(texels, width, height, n_refine, (uint64_t*)out_blocks);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return NTBC_OK;
+}
+
+namespace {
+bool train_layout(const ntbc_train_arch* a, TrainParams& p) {
+  if (!a || a->n_textures < 1 || a->n_textures > kMaxTex || a->hidden != 64 || a->levels < 1 ||
+      a->levels > kMaxLevels || a->coarsest < 2 || ((long long)a->coarsest << (a->levels - 1)) > 8192)
+    return false;
+  p.n_tex = a->n_textures;
+  p.n_c = p.n_e = 0;
+  for (int k = 0; k < p.n_tex; k++) {
+    if (a->fmt[k] != NTBC_BC1 && a->fmt[k] != NTBC_BC4) return false;
+    p.fmt[k] = a->fmt[k];
+    p.n_c += a->fmt[k] == NTBC_BC1 ? 3 : 1;
+    p.n_e += a->fmt[k] == NTBC_BC1 ? 6 : 2;
+  }
+  p.hidden = a->hidden;
+  p.levels = a->levels;
+  p.coarsest = a->coarsest;
+  long long off = 0;
+  for (int l = 0; l < p.levels; l++) {
+    p.lvl_off[l] = off;
+    const long long res = (long long)p.coarsest << l;
+    off += res * res * 2;
+  }
+  const int dims[5] = {2 * p.levels, p.hidden, p.hidden, p.hidden, p.n_c};
+  for (int l = 0; l < 4; l++) {
+    p.kin[l] = dims[l];
+    p.kout[l] = dims[l + 1];
+    p.w_off[l] = off;
+    off += (long long)dims[l] * dims[l + 1];
+    p.b_off[l] = off;
+    off += dims[l + 1];
+  }
+  g_train_total = off;
+  return true;
+}
+}  // namespace
+
+long long ntbc_train_param_count(const ntbc_train_arch* arch) {
+  TrainParams p{};
+  if (!train_layout(arch, p)) return -1;
+  return g_train_total;
+}
+
+ntbc_status ntbc_train_colour_step(const ntbc_train_arch* arch, float* params, float* grads, float* adam_m,
+                                   float* adam_v, int step, const int* xy, const float* cref, const float* eref,
+                                   int batch, int width, int height, float temperature, float lr_grid,
+                                   float lr_mlp, float* loss, void* stream) {
+  TrainParams p{};
+  if (!train_layout(arch, p)) return fail(NTBC_EINVAL, "unsupported training architecture (hidden must be 64)");
+  const long long n = g_train_total, n_grid = p.w_off[0];
+  if (!params || !grads || !adam_m || !adam_v || !xy || !cref || !eref || !loss) return fail(NTBC_EINVAL, "NULL argument");
+  if (batch < 1 || width < 1 || height < 1 || step < 1 || !(temperature > 0.0f)) return fail(NTBC_EINVAL, "bad batch/size/step/T");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(grads, 0, (size_t)n * sizeof(float), st));
+  CUDA_TRY(cudaMemsetAsync(loss, 0, sizeof(float), st));
+  p.params = params; p.grads = grads; p.xy = xy; p.cref = cref; p.eref = eref;
+  p.B = batch; p.W = width; p.H = height; p.T = temperature; p.loss = loss;
+  size_t smem = 0;
+  for (int l = 0; l < 4; l++) smem += (size_t)(p.kin[l] * p.kout[l] + p.kout[l]);
+  smem += (size_t)kTrainTile * (2 * p.levels + 1) + 4 * (size_t)kTrainTile * 65 + kTrainTile;
+  smem *= sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    CUDA_TRY(cudaFuncSetAttribute(train_colour_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  train_colour_kernel<64><<<(batch + kTrainTile - 1) / kTrainTile, kTrainTile, smem, st>>>(p);
+  g_launches++;
+  const double bc1 = 1.0 - std::pow(0.9, step), bc2 = 1.0 - std::pow(0.999, step);
+  const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 32);
+  adam_kernel<<<grid, 256, 0, st>>>(params, grads, adam_m, adam_v, n, n_grid, lr_grid, lr_mlp, 0.9f, 0.999f, 1e-15f,
+                                    (float)bc1, (float)bc2);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return NTBC_OK;

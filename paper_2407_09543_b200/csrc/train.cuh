@@ -1,0 +1,244 @@
+// train.cuh -- one training step of the NTBC colour network on sm_100a.
+//
+// PAPER.md: loss L_color = L_c + L_cd (Eq. 14-15) with the colour-network index rule
+// (P:274-285), STE through the argmax as the softmax expectation (App. A, T = 0.01), Adam
+// with separate grid / MLP learning rates.  DESIGN.md R30-R32 fix the parameter layout,
+// the batch-mean loss and this implementation's precision (fp32 throughout, CUDA cores).
+//
+// Kernel (1) train_colour_kernel: one CTA = 128 texel samples, one thread per sample.  The MLP
+// weights live in shared memory; the layer inputs of the tile (features, three hidden activations)
+// are kept in shared memory for the backward pass (selu' is recovered from the activation:
+// lambda for a > 0, a + lambda*alpha otherwise).  Weight gradients are reduced over the tile in
+// shared memory and added to the global gradient with one atomic per weight per CTA; the grid
+// gradient is scattered with atomics (4 vertices x 2 features per level per sample).
+// Kernel (2) adam_kernel: bias-corrected Adam over the flat parameter vector.
+#pragma once
+#include <cstdint>
+
+namespace ntbc {
+
+constexpr int kTrainTile = 128;
+constexpr float kSeluL = 1.0507009873554804934f, kSeluLA = 1.0507009873554804934f * 1.6732632423543772848f;
+
+struct TrainParams {
+  int n_tex, fmt[kMaxTex], hidden, levels, coarsest, n_c, n_e;
+  long long lvl_off[kMaxLevels];      // offsets (floats) of the grid levels in the parameter vector
+  long long w_off[4], b_off[4];       // offsets of W_l [in][out] and b_l [out]
+  int kin[4], kout[4];
+  const float* params;
+  float* grads;
+  const int* xy;                      // [B][2] texel coordinates
+  const float* cref;                  // [B][n_c] reference colours
+  const float* eref;                  // [B][n_e] reference endpoints (BC1: e0 rgb, e1 rgb; BC4: e0, e1)
+  int B, W, H;
+  float T;
+  float* loss;                        // += batch-mean loss
+};
+
+__device__ __forceinline__ float selu_f(float z) { return z > 0.0f ? kSeluL * z : kSeluLA * (expf(z) - 1.0f); }
+
+// reference palette of one texture (Eq. 7 / Eq. 8), linear order: BC1 4 x 3, BC4 8 x 1
+__device__ __forceinline__ int train_palette(int fmt, const float* e, float* pal) {
+  if (fmt == kFmtBC1) {
+    for (int n = 0; n < 4; n++) {
+      const float w = (float)n / 3.0f;
+      for (int c = 0; c < 3; c++) pal[3 * n + c] = (1.0f - w) * e[c] + w * e[3 + c];
+    }
+    return 4;
+  }
+  if (e[0] > e[1]) {
+    for (int n = 0; n < 8; n++) { const float w = (float)n / 7.0f; pal[n] = (1.0f - w) * e[0] + w * e[1]; }
+  } else {
+    pal[0] = 0.0f;
+    for (int n = 1; n <= 6; n++) { const float w = (float)(n - 1) / 5.0f; pal[n] = (1.0f - w) * e[0] + w * e[1]; }
+    pal[7] = 1.0f;
+  }
+  return 8;
+}
+
+template <int HID>
+__global__ void __launch_bounds__(kTrainTile, 1) train_colour_kernel(const __grid_constant__ TrainParams p) {
+  extern __shared__ float sm[];
+  const int tid = threadIdx.x, n_c = p.n_c, F = 2 * p.levels;
+  constexpr int LD = HID + 1;                                   // padded row stride (bank-conflict free)
+  // ---- shared memory: weights, biases, tile activations A0 (features), A1..A3, delta buffer
+  float* sW[4];
+  float* sb[4];
+  float* q = sm;
+  for (int l = 0; l < 4; l++) { sW[l] = q; q += p.kin[l] * p.kout[l]; sb[l] = q; q += p.kout[l]; }
+  float* A[4];
+  A[0] = q; q += kTrainTile * (F + 1);
+  for (int l = 1; l < 4; l++) { A[l] = q; q += kTrainTile * LD; }
+  float* Dl = q; q += kTrainTile * LD;                          // delta of the current layer output
+  float* red = q;                                               // [kTrainTile] loss reduction
+  const int ldA[4] = {F + 1, LD, LD, LD};
+  for (int l = 0; l < 4; l++) {
+    const int nw = p.kin[l] * p.kout[l];
+    for (int t = tid; t < nw; t += kTrainTile) sW[l][t] = p.params[p.w_off[l] + t];
+    for (int t = tid; t < p.kout[l]; t += kTrainTile) sb[l][t] = p.params[p.b_off[l] + t];
+  }
+  __syncthreads();
+
+  const int s = blockIdx.x * kTrainTile + tid;
+  const bool valid = s < p.B;
+  const int sc = valid ? s : p.B - 1;
+  const float u = ((float)p.xy[2 * sc] + 0.5f) / (float)p.W, v = ((float)p.xy[2 * sc + 1] + 0.5f) / (float)p.H;
+
+  // ---- forward: grid features (R1-R3), hidden layers, sigmoid outputs
+  for (int l = 0; l < p.levels; l++) {
+    const int res = p.coarsest << l;
+    const float X = u * (float)(res - 1), Y = v * (float)(res - 1);
+    const int i0 = min((int)floorf(X), res - 2), j0 = min((int)floorf(Y), res - 2);
+    const float fx = X - (float)i0, fy = Y - (float)j0;
+    const float* g = p.params + p.lvl_off[l];
+    for (int f = 0; f < 2; f++) {
+      const float v00 = g[((size_t)j0 * res + i0) * 2 + f], v10 = g[((size_t)j0 * res + i0 + 1) * 2 + f];
+      const float v01 = g[((size_t)(j0 + 1) * res + i0) * 2 + f], v11 = g[((size_t)(j0 + 1) * res + i0 + 1) * 2 + f];
+      const float top = v00 + fx * (v10 - v00), bot = v01 + fx * (v11 - v01);
+      A[0][tid * ldA[0] + 2 * l + f] = top + fy * (bot - top);
+    }
+  }
+  for (int l = 0; l < 3; l++) {
+    const float* a = A[l] + tid * ldA[l];
+    float* o = A[l + 1] + tid * LD;
+    for (int j = 0; j < HID; j++) {
+      float z = sb[l][j];
+      for (int k = 0; k < p.kin[l]; k++) z += a[k] * sW[l][k * HID + j];
+      o[j] = selu_f(z);
+    }
+  }
+  float chat[3 * kMaxTex], g_out[3 * kMaxTex];
+  {
+    const float* a = A[3] + tid * LD;
+    for (int j = 0; j < n_c; j++) {
+      float z = sb[3][j];
+      for (int k = 0; k < HID; k++) z += a[k] * sW[3][k * n_c + j];
+      chat[j] = 1.0f / (1.0f + expf(-z));
+    }
+  }
+
+  // ---- loss and dL/dc_hat per texture: L_c + L_cd with the STE expectation (App. A)
+  float loss = 0.0f;
+  {
+    int co = 0, eo = 0;
+    const float invB = 1.0f / (float)p.B, invT = 1.0f / p.T;
+    for (int k = 0; k < p.n_tex; k++) {
+      const int w = p.fmt[k] == kFmtBC1 ? 3 : 1;
+      float pal[24], e[6], c[3], ch[3];
+      for (int t = 0; t < 2 * w; t++) e[t] = p.eref[(size_t)sc * p.n_e + eo + t];
+      for (int t = 0; t < w; t++) { c[t] = p.cref[(size_t)sc * n_c + co + t]; ch[t] = chat[co + t]; }
+      const int nn = train_palette(p.fmt[k], e, pal);
+      float dist[8], dmax = -1e30f;
+      int best = 0;
+      for (int n = 0; n < nn; n++) {
+        float s2 = 0.0f;
+        for (int t = 0; t < w; t++) { const float d = ch[t] - pal[n * w + t]; s2 += d * d; }
+        dist[n] = sqrtf(fmaxf(s2, 1e-30f));
+        if (-dist[n] > dmax) { dmax = -dist[n]; best = n; }        // argmax of d_n = -dist, ties -> lower n
+      }
+      float sig[8], ssum = 0.0f;
+      for (int n = 0; n < nn; n++) { sig[n] = expf((-dist[n] - dmax) * invT); ssum += sig[n]; }
+      for (int n = 0; n < nn; n++) sig[n] /= ssum;
+      // forward values: L_c = |c_hat - c|^2, L_cd = |c_n(best) - c|^2
+      float G[8], gd[3];
+      for (int t = 0; t < w; t++) {
+        const float dc = ch[t] - c[t], dd = pal[best * w + t] - c[t];
+        loss += dc * dc + dd * dd;
+        gd[t] = 2.0f * dd;                                         // dL/dc_dec (forward value)
+      }
+      float sG = 0.0f;
+      for (int n = 0; n < nn; n++) {                               // G_n = dL/dc_dec . c_n
+        G[n] = 0.0f;
+        for (int t = 0; t < w; t++) G[n] += gd[t] * pal[n * w + t];
+        sG += sig[n] * G[n];
+      }
+      for (int x = 0; x < w; x++) {
+        // d soft / d c_hat_x = (1/T) sum_n sigma_n (G_n - sum_m sigma_m G_m) dd_n/dc_hat_x,
+        // dd_n / dc_hat_x = -(c_hat_x - c_n,x) / dist_n
+        float acc = 0.0f;
+        for (int n = 0; n < nn; n++) acc += sig[n] * (G[n] - sG) * (-(ch[x] - pal[n * w + x]) / dist[n]);
+        const float gx = 2.0f * (ch[x] - c[x]) + invT * acc;
+        g_out[co + x] = valid ? gx * invB * ch[x] * (1.0f - ch[x]) : 0.0f;   // through the sigmoid
+      }
+      co += w;
+      eo += 2 * w;
+    }
+  }
+  red[tid] = valid ? loss : 0.0f;
+
+  // ---- backward: output layer delta -> D, then layers 3..0
+  float* D = Dl;
+  for (int j = 0; j < n_c; j++) D[tid * LD + j] = g_out[j];
+  __syncthreads();
+  for (int l = 3; l >= 0; l--) {
+    const int K = p.kin[l], N = p.kout[l];
+    // weight and bias gradients of layer l over the tile: dW[k][j] = sum_i A_l[i][k] D[i][j]
+    for (int e = tid; e < K * N + N; e += kTrainTile) {
+      float acc = 0.0f;
+      if (e < K * N) {
+        const int k = e / N, j = e - k * N;
+        for (int i = 0; i < kTrainTile; i++) acc += A[l][i * ldA[l] + k] * D[i * LD + j];
+        atomicAdd(p.grads + p.w_off[l] + e, acc);
+      } else {
+        const int j = e - K * N;
+        for (int i = 0; i < kTrainTile; i++) acc += D[i * LD + j];
+        atomicAdd(p.grads + p.b_off[l] + j, acc);
+      }
+    }
+    // delta of this layer's input: dA[k] = sum_j W[k][j] D[j]; through selu' for hidden inputs
+    float dA[HID];
+    for (int k = 0; k < K; k++) {
+      float acc = 0.0f;
+      for (int j = 0; j < N; j++) acc += sW[l][k * N + j] * D[tid * LD + j];
+      if (l > 0) {
+        const float a = A[l][tid * ldA[l] + k];
+        acc *= a > 0.0f ? kSeluL : a + kSeluLA;                     // selu'(z) from a = selu(z)
+      }
+      dA[k] = acc;
+    }
+    __syncthreads();                                               // all readers of D are done
+    for (int k = 0; k < K; k++) D[tid * LD + k] = dA[k];
+    __syncthreads();
+  }
+  // ---- grid gradient: scatter d features through the bilinear weights of each level
+  if (valid) {
+    for (int l = 0; l < p.levels; l++) {
+      const int res = p.coarsest << l;
+      const float X = u * (float)(res - 1), Y = v * (float)(res - 1);
+      const int i0 = min((int)floorf(X), res - 2), j0 = min((int)floorf(Y), res - 2);
+      const float fx = X - (float)i0, fy = Y - (float)j0;
+      float* g = p.grads + p.lvl_off[l];
+      for (int f = 0; f < 2; f++) {
+        const float d = D[tid * LD + 2 * l + f];
+        atomicAdd(g + ((size_t)j0 * res + i0) * 2 + f, d * (1.0f - fx) * (1.0f - fy));
+        atomicAdd(g + ((size_t)j0 * res + i0 + 1) * 2 + f, d * fx * (1.0f - fy));
+        atomicAdd(g + ((size_t)(j0 + 1) * res + i0) * 2 + f, d * (1.0f - fx) * fy);
+        atomicAdd(g + ((size_t)(j0 + 1) * res + i0 + 1) * 2 + f, d * fx * fy);
+      }
+    }
+  }
+  // ---- batch-mean loss
+  __syncthreads();
+  for (int st = kTrainTile / 2; st > 0; st >>= 1) {
+    if (tid < st) red[tid] += red[tid + st];
+    __syncthreads();
+  }
+  if (tid == 0) atomicAdd(p.loss, red[0] / (float)p.B);
+}
+
+// bias-corrected Adam: lr_grid for the first n_grid parameters, lr_mlp for the rest
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, const float* __restrict__ grads,
+                                                   float* __restrict__ m, float* __restrict__ v, long long n,
+                                                   long long n_grid, float lr_grid, float lr_mlp, float beta1,
+                                                   float beta2, float eps, float bc1, float bc2) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float g = grads[i];
+    const float mi = beta1 * m[i] + (1.0f - beta1) * g, vi = beta2 * v[i] + (1.0f - beta2) * g * g;
+    m[i] = mi;
+    v[i] = vi;
+    const float lr = i < n_grid ? lr_grid : lr_mlp;
+    params[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  }
+}
+
+}  // namespace ntbc

@@ -41,6 +41,9 @@ _SIGS = {
     "ntbc_decode_material_host": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _vp]),
     "ntbc_decode_bc": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "ntbc_encode_bc": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
+    "ntbc_train_param_count": (C.c_longlong, [_vp]),
+    "ntbc_train_colour_step": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _i, C.c_float, C.c_float,
+                                    C.c_float, _vp, _vp]),
     "ntbc_debug_mlp": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ntbc_debug_features": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ntbc_pack": (_i, [_i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
@@ -150,6 +153,41 @@ def encode_bc(texels: torch.Tensor, fmt: int, width: int, height: int, n_refine:
         out = torch.empty((height // 4, width // 4), dtype=torch.int64, device=texels.device)
     _check(_lib.ntbc_encode_bc(texels.data_ptr(), fmt, width, height, n_refine, out.data_ptr(), _stream(stream)))
     return out
+
+
+class _TrainArch(C.Structure):
+    _fields_ = [("n_textures", C.c_int), ("fmt", C.c_int * 8), ("hidden", C.c_int), ("levels", C.c_int),
+                ("coarsest", C.c_int)]
+
+
+def _train_arch(fmts, hidden, levels, coarsest):
+    a = _TrainArch()
+    a.n_textures = len(fmts)
+    for i, f in enumerate(fmts):
+        a.fmt[i] = f
+    a.hidden, a.levels, a.coarsest = hidden, levels, coarsest
+    return a
+
+
+def train_param_count(fmts, hidden=64, levels=8, coarsest=16) -> int:
+    n = int(_lib.ntbc_train_param_count(C.byref(_train_arch(fmts, hidden, levels, coarsest))))
+    if n < 0:
+        raise NtbcError(-1, "unsupported training architecture")
+    return n
+
+
+def train_colour_step(fmts, params, grads, adam_m, adam_v, step, xy, cref, eref, width, height,
+                      temperature=0.01, lr_grid=0.01, lr_mlp=0.005, hidden=64, levels=8, coarsest=16,
+                      loss=None, stream=None):
+    """ntbc_train_colour_step on device fp32 tensors (params/grads/adam_m/adam_v: flat; xy int32 [B][2])."""
+    if loss is None:
+        loss = torch.zeros(1, dtype=torch.float32, device=params.device)
+    arch = _train_arch(fmts, hidden, levels, coarsest)
+    _check(_lib.ntbc_train_colour_step(C.byref(arch), params.data_ptr(), grads.data_ptr(), adam_m.data_ptr(),
+                                       adam_v.data_ptr(), step, xy.data_ptr(), cref.data_ptr(), eref.data_ptr(),
+                                       xy.shape[0], width, height, temperature, lr_grid, lr_mlp, loss.data_ptr(),
+                                       _stream(stream)))
+    return loss
 
 
 def decode_bc(blocks: torch.Tensor, fmt: int, width: int, height: int, out=None, stream=None):

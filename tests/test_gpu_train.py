@@ -1,0 +1,77 @@
+"""GPU parity of the colour-network training step (-m gpu): ntbc_train_colour_step
+(fp32, CUDA cores, atomic accumulation) against the float64 autograd oracle (oracle/train_oracle.py).
+
+Bars (R32): loss within 1e-5 relative; every parameter class (grid levels, weights,
+biases) of the gradient within tol x the norm of the whole gradient, tol = 1e-5 / T (fp32 terms of
+the STE expectation carry a 1/T factor, and grid entries are sums of many sample contributions with
+cancellation, accumulated by atomics in arbitrary order); the Adam update equal (1e-6 relative) to
+the bias-corrected formula applied to the GPU's own gradient.  A wrong sign, factor or index in any
+term is an O(1) relative error."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import train_oracle as T
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def ntbc():
+    from paper_2407_09543_b200 import ntbc as n
+    return n
+
+
+def _case(fmts, levels, coarsest, B, seed, W=256, H=192):
+    rng = np.random.default_rng(seed)
+    lay = T.layout(fmts, 64, levels, coarsest)
+    n = sum(int(np.prod(s)) for _, s in lay)
+    n_grid = sum(int(np.prod(s)) for nme, s in lay if nme.startswith("grid"))
+    p = rng.standard_normal(n) * 0.3
+    p[:n_grid] = rng.uniform(-1, 1, n_grid)
+    n_c = sum(3 if f == T.BC1 else 1 for f in fmts)
+    n_e = sum(6 if f == T.BC1 else 2 for f in fmts)
+    xy = np.stack([rng.integers(0, W, B), rng.integers(0, H, B)], 1).astype(np.int32)
+    cref = rng.uniform(0, 1, (B, n_c))
+    eref = rng.uniform(0, 1, (B, n_e))
+    return lay, n_grid, p.astype(np.float32), xy, cref.astype(np.float32), eref.astype(np.float32), W, H
+
+
+@pytest.mark.parametrize("fmts,levels,coarsest,B,temp", [
+    ([T.BC1, T.BC4], 2, 4, 300, 0.1),
+    ([T.BC1, T.BC1, T.BC4, T.BC4, T.BC4], 4, 8, 1000, 0.01),
+    ([T.BC4, T.BC1], 8, 16, 2048, 0.01),                     # the paper's texel grid
+])
+def test_train_step_matches_oracle(ntbc, fmts, levels, coarsest, B, temp):
+    lay, n_grid, p, xy, cref, eref, W, H = _case(fmts, levels, coarsest, B, seed=B)
+    n = p.size
+    assert ntbc.train_param_count(fmts, 64, levels, coarsest) == n
+    dp = torch.from_numpy(p).to(DEV)
+    g = torch.zeros(n, device=DEV)
+    m = torch.zeros(n, device=DEV)
+    v = torch.zeros(n, device=DEV)
+    loss = ntbc.train_colour_step(fmts, dp, g, m, v, 1, torch.from_numpy(xy).to(DEV), torch.from_numpy(cref).to(DEV),
+                                  torch.from_numpy(eref).to(DEV), W, H, temperature=temp, levels=levels,
+                                  coarsest=coarsest)
+    torch.cuda.synchronize()
+    ref_loss, ref_g, _, _, _ = T.colour_step(torch.from_numpy(p.astype(np.float64)), torch.zeros(n, dtype=torch.float64),
+                                             torch.zeros(n, dtype=torch.float64), 1, lay, fmts,
+                                             torch.from_numpy(xy.astype(np.int64)), W, H,
+                                             torch.from_numpy(cref.astype(np.float64)),
+                                             torch.from_numpy(eref.astype(np.float64)), T=temp)
+    assert abs(float(loss) - ref_loss) <= 1e-5 * abs(ref_loss)
+    gg = g.double().cpu()
+    off = 0
+    for name, shape in lay:                               # every parameter class separately
+        k = int(np.prod(shape))
+        a, b = gg[off:off + k], ref_g[off:off + k]
+        assert float(torch.linalg.norm(a - b)) <= 1e-5 / temp * float(torch.linalg.norm(ref_g)) + 1e-12, name
+        off += k
+    # Adam update applied to the GPU's own gradient (bias-corrected)
+    lr = torch.full((n,), 0.005, dtype=torch.float64)
+    lr[:n_grid] = 0.01
+    want, _, _ = T.adam(torch.from_numpy(p.astype(np.float64)), gg, torch.zeros(n, dtype=torch.float64),
+                        torch.zeros(n, dtype=torch.float64), 1, lr)
+    got = dp.double().cpu()
+    assert torch.allclose(got, want, rtol=1e-6, atol=1e-7)

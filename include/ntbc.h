@@ -133,6 +133,17 @@ ntbc_status ntbc_train_colour_step(const ntbc_train_arch* arch, float* params, f
                                    float* adam_v, int step, const int* xy, const float* cref, const float* eref,
                                    int batch, int width, int height, float temperature, float lr_grid,
                                    float lr_mlp, float* loss, void* stream);
+/* The endpoint network's step (Eq. 14: L_e + L_cd): parameters = the BLOCK grid levels and
+ * the 2*levels -> hidden x3 -> N_e MLP (same layout rules); samples are blocks: bxy [B][2] block
+ * coordinates (< blocks_w, blocks_h), eref [B][N_e] reference endpoints, cref16 [B][16][N_c] the
+ * reference colours of the block's texels (texel i = 4y + x).  Each texel's index comes from the
+ * PREDICTED endpoints' palette and its reference colour; the decoded colour is the REFERENCE
+ * endpoints' palette entry at that index; STE and Adam as above. */
+long long ntbc_train_endpoint_param_count(const ntbc_train_arch* arch);
+ntbc_status ntbc_train_endpoint_step(const ntbc_train_arch* arch, float* params, float* grads, float* adam_m,
+                                     float* adam_v, int step, const int* bxy, const float* cref16, const float* eref,
+                                     int batch, int blocks_w, int blocks_h, float temperature, float lr_grid,
+                                     float lr_mlp, float* loss, void* stream);
 
 /* Row a9 (verification): decode a BC1/BC4 surface with the DirectX palettes (decode uses
  * the same float palette arithmetic as the encoder, R18) into fp32 texels.

@@ -132,3 +132,59 @@ def colour_step(params, m, v, step, lay, fmts, xy, W, H, cref, eref, T=0.01, lr_
     lr[:n_grid] = lr_grid
     p2, m2, v2 = adam(params, g, m, v, step, lr)
     return float(loss.detach()), g, p2, m2, v2
+
+
+# ---------------------------------------------------------------- endpoint network (Eq. 14)
+def layout_endpoint(fmts, hidden, levels, coarsest):
+    """Flat parameter vector of the endpoint network: block grid levels, then the MLP to N_e outputs."""
+    n_e = sum(6 if f == BC1 else 2 for f in fmts)
+    out = [(f"grid{l}", (coarsest << l, coarsest << l, 2)) for l in range(levels)]
+    dims = [2 * levels, hidden, hidden, hidden, n_e]
+    for l in range(4):
+        out += [(f"W{l}", (dims[l], dims[l + 1])), (f"b{l}", (dims[l + 1],))]
+    return out
+
+
+def endpoint_loss(params, lay, fmts, bxy, BW, BH, eref, cref16, T):
+    """L_endpoint = L_e + L_cd (Eq. 14), batch mean.  eref [B][N_e] reference endpoints, cref16
+    [B][16][N_c] reference colours of the block's texels (texel i = 4y + x).  The index of each texel
+    comes from the PREDICTED endpoints' palette and the reference colour; the decoded colour is the
+    REFERENCE endpoints' palette entry at that index; STE as for the colour network."""
+    p = unflatten(params, lay)
+    levels = sum(1 for name, _ in lay if name.startswith("grid"))
+    s = (bxy[:, 0].double() + 0.5) / BW
+    t = (bxy[:, 1].double() + 0.5) / BH
+    a = grid_features([p[f"grid{l}"] for l in range(levels)], s, t)
+    for l in range(3):
+        a = torch.nn.functional.selu(a @ p[f"W{l}"] + p[f"b{l}"])
+    ehat = torch.sigmoid(a @ p["W3"] + p["b3"])
+    loss = ((ehat - eref) ** 2).sum()
+    eo = co = 0
+    B = bxy.shape[0]
+    for f in fmts:
+        w, we = (3, 6) if f == BC1 else (1, 2)
+        pal_pred = palettes(f, ehat[:, eo:eo + we])            # [B][n][w], differentiable in ehat
+        pal_ref = palettes(f, eref[:, eo:eo + we])
+        for i in range(16):
+            c = cref16[:, i, co:co + w]
+            dist = torch.sqrt(torch.clamp(((c[:, None, :] - pal_pred) ** 2).sum(-1), min=1e-30))
+            d = -dist
+            n = torch.argmax(d, dim=1)
+            hard = pal_ref[torch.arange(B), n]
+            soft = (torch.softmax(d / T, dim=1)[:, :, None] * pal_ref).sum(1)
+            dec = soft + (hard - soft).detach()
+            loss = loss + ((dec - c) ** 2).sum()
+        eo += we
+        co += w
+    return loss / B
+
+
+def endpoint_step(params, m, v, step, lay, fmts, bxy, BW, BH, eref, cref16, T=0.01, lr_grid=0.01, lr_mlp=0.005):
+    x = params.clone().requires_grad_(True)
+    loss = endpoint_loss(x, lay, fmts, bxy, BW, BH, eref, cref16, T)
+    (g,) = torch.autograd.grad(loss, x)
+    n_grid = sum(int(np.prod(s)) for name, s in lay if name.startswith("grid"))
+    lr = torch.full_like(params, lr_mlp)
+    lr[:n_grid] = lr_grid
+    p2, m2, v2 = adam(params, g, m, v, step, lr)
+    return float(loss.detach()), g, p2, m2, v2

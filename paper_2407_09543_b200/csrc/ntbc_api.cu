@@ -623,7 +623,7 @@ ntbc_status ntbc_encode_bc(const float* texels, ntbc_format fmt, int width, int 
 }
 
 namespace {
-bool train_layout(const ntbc_train_arch* a, TrainParams& p) {
+bool train_layout(const ntbc_train_arch* a, TrainParams& p, int net) {
   if (!a || a->n_textures < 1 || a->n_textures > kMaxTex || a->hidden != 64 || a->levels < 1 ||
       a->levels > kMaxLevels || a->coarsest < 2 || ((long long)a->coarsest << (a->levels - 1)) > 8192)
     return false;
@@ -644,7 +644,7 @@ bool train_layout(const ntbc_train_arch* a, TrainParams& p) {
     const long long res = (long long)p.coarsest << l;
     off += res * res * 2;
   }
-  const int dims[5] = {2 * p.levels, p.hidden, p.hidden, p.hidden, p.n_c};
+  const int dims[5] = {2 * p.levels, p.hidden, p.hidden, p.hidden, net == 1 ? p.n_c : p.n_e};
   for (int l = 0; l < 4; l++) {
     p.kin[l] = dims[l];
     p.kout[l] = dims[l + 1];
@@ -660,16 +660,23 @@ bool train_layout(const ntbc_train_arch* a, TrainParams& p) {
 
 long long ntbc_train_param_count(const ntbc_train_arch* arch) {
   TrainParams p{};
-  if (!train_layout(arch, p)) return -1;
+  if (!train_layout(arch, p, 1)) return -1;
   return g_train_total;
 }
 
-ntbc_status ntbc_train_colour_step(const ntbc_train_arch* arch, float* params, float* grads, float* adam_m,
-                                   float* adam_v, int step, const int* xy, const float* cref, const float* eref,
-                                   int batch, int width, int height, float temperature, float lr_grid,
-                                   float lr_mlp, float* loss, void* stream) {
+long long ntbc_train_endpoint_param_count(const ntbc_train_arch* arch) {
   TrainParams p{};
-  if (!train_layout(arch, p)) return fail(NTBC_EINVAL, "unsupported training architecture (hidden must be 64)");
+  if (!train_layout(arch, p, 0)) return -1;
+  return g_train_total;
+}
+
+namespace {
+ntbc_status train_step(int net, const ntbc_train_arch* arch, float* params, float* grads, float* adam_m,
+                       float* adam_v, int step, const int* xy, const float* cref, const float* eref, int batch,
+                       int width, int height, float temperature, float lr_grid, float lr_mlp, float* loss,
+                       void* stream) {
+  TrainParams p{};
+  if (!train_layout(arch, p, net)) return fail(NTBC_EINVAL, "unsupported training architecture (hidden must be 64)");
   const long long n = g_train_total, n_grid = p.w_off[0];
   if (!params || !grads || !adam_m || !adam_v || !xy || !cref || !eref || !loss) return fail(NTBC_EINVAL, "NULL argument");
   if (batch < 1 || width < 1 || height < 1 || step < 1 || !(temperature > 0.0f)) return fail(NTBC_EINVAL, "bad batch/size/step/T");
@@ -682,12 +689,13 @@ ntbc_status ntbc_train_colour_step(const ntbc_train_arch* arch, float* params, f
   for (int l = 0; l < 4; l++) smem += (size_t)(p.kin[l] * p.kout[l] + p.kout[l]);
   smem += (size_t)kTrainTile * (2 * p.levels + 1) + 4 * (size_t)kTrainTile * 65 + kTrainTile;
   smem *= sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    CUDA_TRY(cudaFuncSetAttribute(train_colour_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
+  auto kern = net == 1 ? train_step_kernel<64, 1> : train_step_kernel<64, 0>;
+  static bool configured[2] = {false, false};
+  if (!configured[net]) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured[net] = true;
   }
-  train_colour_kernel<64><<<(batch + kTrainTile - 1) / kTrainTile, kTrainTile, smem, st>>>(p);
+  kern<<<(batch + kTrainTile - 1) / kTrainTile, kTrainTile, smem, st>>>(p);
   g_launches++;
   const double bc1 = 1.0 - std::pow(0.9, step), bc2 = 1.0 - std::pow(0.999, step);
   const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 32);
@@ -696,6 +704,23 @@ ntbc_status ntbc_train_colour_step(const ntbc_train_arch* arch, float* params, f
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return NTBC_OK;
+}
+}  // namespace
+
+ntbc_status ntbc_train_colour_step(const ntbc_train_arch* arch, float* params, float* grads, float* adam_m,
+                                   float* adam_v, int step, const int* xy, const float* cref, const float* eref,
+                                   int batch, int width, int height, float temperature, float lr_grid,
+                                   float lr_mlp, float* loss, void* stream) {
+  return train_step(1, arch, params, grads, adam_m, adam_v, step, xy, cref, eref, batch, width, height, temperature,
+                    lr_grid, lr_mlp, loss, stream);
+}
+
+ntbc_status ntbc_train_endpoint_step(const ntbc_train_arch* arch, float* params, float* grads, float* adam_m,
+                                     float* adam_v, int step, const int* bxy, const float* cref16, const float* eref,
+                                     int batch, int blocks_w, int blocks_h, float temperature, float lr_grid,
+                                     float lr_mlp, float* loss, void* stream) {
+  return train_step(0, arch, params, grads, adam_m, adam_v, step, bxy, cref16, eref, batch, blocks_w, blocks_h,
+                    temperature, lr_grid, lr_mlp, loss, stream);
 }
 
 ntbc_status ntbc_decode_bc(const void* blocks, ntbc_format fmt, int width, int height, float* out, void* stream) {

@@ -28,7 +28,7 @@ struct TrainParams {
   const float* params;
   float* grads;
   const int* xy;                      // [B][2] texel coordinates
-  const float* cref;                  // [B][n_c] reference colours
+  const float* cref;                  // colour net: [B][n_c] reference colours; endpoint net: [B][16][n_c]
   const float* eref;                  // [B][n_e] reference endpoints (BC1: e0 rgb, e1 rgb; BC4: e0, e1)
   int B, W, H;
   float T;
@@ -56,10 +56,20 @@ __device__ __forceinline__ int train_palette(int fmt, const float* e, float* pal
   return 8;
 }
 
-template <int HID>
-__global__ void __launch_bounds__(kTrainTile, 1) train_colour_kernel(const __grid_constant__ TrainParams p) {
+// palette interpolation weight of linear entry n and whether the entry is a constant (BC4 6-value 0/1)
+__device__ __forceinline__ float train_weight(int fmt, bool mode8, int n, bool& constant) {
+  constant = false;
+  if (fmt == kFmtBC1) return (float)n / 3.0f;
+  if (mode8) return (float)n / 7.0f;
+  constant = n == 0 || n == 7;
+  return constant ? 0.0f : (float)(n - 1) / 5.0f;
+}
+
+// NET = 1: colour network (samples are texels); NET = 0: endpoint network (samples are blocks)
+template <int HID, int NET>
+__global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_constant__ TrainParams p) {
   extern __shared__ float sm[];
-  const int tid = threadIdx.x, n_c = p.n_c, F = 2 * p.levels;
+  const int tid = threadIdx.x, n_c = NET ? p.n_c : p.n_e, F = 2 * p.levels;   // n_c here = MLP outputs
   constexpr int LD = HID + 1;                                   // padded row stride (bank-conflict free)
   // ---- shared memory: weights, biases, tile activations A0 (features), A1..A3, delta buffer
   float* sW[4];
@@ -107,7 +117,7 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_colour_kernel(const __gri
       o[j] = selu_f(z);
     }
   }
-  float chat[3 * kMaxTex], g_out[3 * kMaxTex];
+  float chat[6 * kMaxTex], g_out[6 * kMaxTex];
   {
     const float* a = A[3] + tid * LD;
     for (int j = 0; j < n_c; j++) {
@@ -117,54 +127,118 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_colour_kernel(const __gri
     }
   }
 
-  // ---- loss and dL/dc_hat per texture: L_c + L_cd with the STE expectation (App. A)
-  float loss = 0.0f;
-  {
-    int co = 0, eo = 0;
-    const float invB = 1.0f / (float)p.B, invT = 1.0f / p.T;
-    for (int k = 0; k < p.n_tex; k++) {
-      const int w = p.fmt[k] == kFmtBC1 ? 3 : 1;
-      float pal[24], e[6], c[3], ch[3];
-      for (int t = 0; t < 2 * w; t++) e[t] = p.eref[(size_t)sc * p.n_e + eo + t];
-      for (int t = 0; t < w; t++) { c[t] = p.cref[(size_t)sc * n_c + co + t]; ch[t] = chat[co + t]; }
-      const int nn = train_palette(p.fmt[k], e, pal);
-      float dist[8], dmax = -1e30f;
-      int best = 0;
-      for (int n = 0; n < nn; n++) {
-        float s2 = 0.0f;
-        for (int t = 0; t < w; t++) { const float d = ch[t] - pal[n * w + t]; s2 += d * d; }
-        dist[n] = sqrtf(fmaxf(s2, 1e-30f));
-        if (-dist[n] > dmax) { dmax = -dist[n]; best = n; }        // argmax of d_n = -dist, ties -> lower n
+  if constexpr (NET == 1) {
+    // ---- loss and dL/dc_hat per texture: L_c + L_cd with the STE expectation (App. A)
+    float loss = 0.0f;
+    {
+      int co = 0, eo = 0;
+      const float invB = 1.0f / (float)p.B, invT = 1.0f / p.T;
+      for (int k = 0; k < p.n_tex; k++) {
+        const int w = p.fmt[k] == kFmtBC1 ? 3 : 1;
+        float pal[24], e[6], c[3], ch[3];
+        for (int t = 0; t < 2 * w; t++) e[t] = p.eref[(size_t)sc * p.n_e + eo + t];
+        for (int t = 0; t < w; t++) { c[t] = p.cref[(size_t)sc * n_c + co + t]; ch[t] = chat[co + t]; }
+        const int nn = train_palette(p.fmt[k], e, pal);
+        float dist[8], dmax = -1e30f;
+        int best = 0;
+        for (int n = 0; n < nn; n++) {
+          float s2 = 0.0f;
+          for (int t = 0; t < w; t++) { const float d = ch[t] - pal[n * w + t]; s2 += d * d; }
+          dist[n] = sqrtf(fmaxf(s2, 1e-30f));
+          if (-dist[n] > dmax) { dmax = -dist[n]; best = n; }        // argmax of d_n = -dist, ties -> lower n
+        }
+        float sig[8], ssum = 0.0f;
+        for (int n = 0; n < nn; n++) { sig[n] = expf((-dist[n] - dmax) * invT); ssum += sig[n]; }
+        for (int n = 0; n < nn; n++) sig[n] /= ssum;
+        // forward values: L_c = |c_hat - c|^2, L_cd = |c_n(best) - c|^2
+        float G[8], gd[3];
+        for (int t = 0; t < w; t++) {
+          const float dc = ch[t] - c[t], dd = pal[best * w + t] - c[t];
+          loss += dc * dc + dd * dd;
+          gd[t] = 2.0f * dd;                                         // dL/dc_dec (forward value)
+        }
+        float sG = 0.0f;
+        for (int n = 0; n < nn; n++) {                               // G_n = dL/dc_dec . c_n
+          G[n] = 0.0f;
+          for (int t = 0; t < w; t++) G[n] += gd[t] * pal[n * w + t];
+          sG += sig[n] * G[n];
+        }
+        for (int x = 0; x < w; x++) {
+          // d soft / d c_hat_x = (1/T) sum_n sigma_n (G_n - sum_m sigma_m G_m) dd_n/dc_hat_x,
+          // dd_n / dc_hat_x = -(c_hat_x - c_n,x) / dist_n
+          float acc = 0.0f;
+          for (int n = 0; n < nn; n++) acc += sig[n] * (G[n] - sG) * (-(ch[x] - pal[n * w + x]) / dist[n]);
+          const float gx = 2.0f * (ch[x] - c[x]) + invT * acc;
+          g_out[co + x] = valid ? gx * invB * ch[x] * (1.0f - ch[x]) : 0.0f;   // through the sigmoid
+        }
+        co += w;
+        eo += 2 * w;
       }
-      float sig[8], ssum = 0.0f;
-      for (int n = 0; n < nn; n++) { sig[n] = expf((-dist[n] - dmax) * invT); ssum += sig[n]; }
-      for (int n = 0; n < nn; n++) sig[n] /= ssum;
-      // forward values: L_c = |c_hat - c|^2, L_cd = |c_n(best) - c|^2
-      float G[8], gd[3];
-      for (int t = 0; t < w; t++) {
-        const float dc = ch[t] - c[t], dd = pal[best * w + t] - c[t];
-        loss += dc * dc + dd * dd;
-        gd[t] = 2.0f * dd;                                         // dL/dc_dec (forward value)
-      }
-      float sG = 0.0f;
-      for (int n = 0; n < nn; n++) {                               // G_n = dL/dc_dec . c_n
-        G[n] = 0.0f;
-        for (int t = 0; t < w; t++) G[n] += gd[t] * pal[n * w + t];
-        sG += sig[n] * G[n];
-      }
-      for (int x = 0; x < w; x++) {
-        // d soft / d c_hat_x = (1/T) sum_n sigma_n (G_n - sum_m sigma_m G_m) dd_n/dc_hat_x,
-        // dd_n / dc_hat_x = -(c_hat_x - c_n,x) / dist_n
-        float acc = 0.0f;
-        for (int n = 0; n < nn; n++) acc += sig[n] * (G[n] - sG) * (-(ch[x] - pal[n * w + x]) / dist[n]);
-        const float gx = 2.0f * (ch[x] - c[x]) + invT * acc;
-        g_out[co + x] = valid ? gx * invB * ch[x] * (1.0f - ch[x]) : 0.0f;   // through the sigmoid
-      }
-      co += w;
-      eo += 2 * w;
     }
-  }
   red[tid] = valid ? loss : 0.0f;
+  } else {
+  // ---- endpoint network: L_e + L_cd (Eq. 14); indices from the PREDICTED palette and the reference
+    //      colours, decoded colour from the REFERENCE palette, STE as for the colour net
+    float loss = 0.0f;
+    {
+      const float invB = 1.0f / (float)p.B, invT = 1.0f / p.T;
+      for (int j = 0; j < n_c; j++) {
+        const float d = chat[j] - p.eref[(size_t)sc * n_c + j];
+        loss += d * d;
+        g_out[j] = 2.0f * d;
+      }
+      int co = 0, eo = 0;
+      for (int k = 0; k < p.n_tex; k++) {
+        const int w = p.fmt[k] == kFmtBC1 ? 3 : 1;
+        float pp[24], pr[24], ep[6], er[6];
+        for (int t = 0; t < 2 * w; t++) { ep[t] = chat[eo + t]; er[t] = p.eref[(size_t)sc * n_c + eo + t]; }
+        const int nn = train_palette(p.fmt[k], ep, pp);
+        train_palette(p.fmt[k], er, pr);
+        const bool mode8 = p.fmt[k] == kFmtBC1 || ep[0] > ep[1];
+        for (int i = 0; i < 16; i++) {
+          float c[3];
+          for (int t = 0; t < w; t++) c[t] = p.cref[((size_t)sc * 16 + i) * p.n_c + co + t];
+          float dist[8], dmax = -1e30f;
+          int best = 0;
+          for (int n = 0; n < nn; n++) {
+            float s2 = 0.0f;
+            for (int t = 0; t < w; t++) { const float d = c[t] - pp[n * w + t]; s2 += d * d; }
+            dist[n] = sqrtf(fmaxf(s2, 1e-30f));
+            if (-dist[n] > dmax) { dmax = -dist[n]; best = n; }
+          }
+          float sig[8], ssum = 0.0f;
+          for (int n = 0; n < nn; n++) { sig[n] = expf((-dist[n] - dmax) * invT); ssum += sig[n]; }
+          for (int n = 0; n < nn; n++) sig[n] /= ssum;
+          float gd[3], G[8], sG = 0.0f;
+          for (int t = 0; t < w; t++) {
+            const float dd = pr[best * w + t] - c[t];
+            loss += dd * dd;
+            gd[t] = 2.0f * dd;
+          }
+          for (int n = 0; n < nn; n++) {
+            G[n] = 0.0f;
+            for (int t = 0; t < w; t++) G[n] += gd[t] * pr[n * w + t];
+            sG += sig[n] * G[n];
+          }
+          for (int n = 0; n < nn; n++) {
+            bool constant;
+            const float wn = train_weight(p.fmt[k], mode8, n, constant);
+            if (constant) continue;
+            const float coef = invT * sig[n] * (G[n] - sG);        // dL/dd_n
+            for (int x = 0; x < w; x++) {
+              const float dpal = coef * (-(pp[n * w + x] - c[x]) / dist[n]);   // dL/d pal_pred[n][x]
+              g_out[eo + x] += dpal * (1.0f - wn);
+              g_out[eo + w + x] += dpal * wn;
+            }
+          }
+        }
+        co += w;
+        eo += 2 * w;
+      }
+      for (int j = 0; j < n_c; j++) g_out[j] = valid ? g_out[j] * invB * chat[j] * (1.0f - chat[j]) : 0.0f;
+    }
+  red[tid] = valid ? loss : 0.0f;
+  }
 
   // ---- backward: output layer delta -> D, then layers 3..0
   float* D = Dl;

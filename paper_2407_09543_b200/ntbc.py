@@ -42,6 +42,9 @@ _SIGS = {
     "ntbc_decode_bc": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "ntbc_encode_bc": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
     "ntbc_train_param_count": (C.c_longlong, [_vp]),
+    "ntbc_train_endpoint_param_count": (C.c_longlong, [_vp]),
+    "ntbc_train_endpoint_step": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _i, C.c_float, C.c_float,
+                                      C.c_float, _vp, _vp]),
     "ntbc_train_colour_step": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _i, C.c_float, C.c_float,
                                     C.c_float, _vp, _vp]),
     "ntbc_debug_mlp": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
@@ -187,6 +190,27 @@ def train_colour_step(fmts, params, grads, adam_m, adam_v, step, xy, cref, eref,
                                        adam_v.data_ptr(), step, xy.data_ptr(), cref.data_ptr(), eref.data_ptr(),
                                        xy.shape[0], width, height, temperature, lr_grid, lr_mlp, loss.data_ptr(),
                                        _stream(stream)))
+    return loss
+
+
+def train_endpoint_param_count(fmts, hidden=64, levels=7, coarsest=16) -> int:
+    n = int(_lib.ntbc_train_endpoint_param_count(C.byref(_train_arch(fmts, hidden, levels, coarsest))))
+    if n < 0:
+        raise NtbcError(-1, "unsupported training architecture")
+    return n
+
+
+def train_endpoint_step(fmts, params, grads, adam_m, adam_v, step, bxy, cref16, eref, blocks_w, blocks_h,
+                        temperature=0.01, lr_grid=0.01, lr_mlp=0.005, hidden=64, levels=7, coarsest=16,
+                        loss=None, stream=None):
+    """ntbc_train_endpoint_step: bxy int32 [B][2] block coords, cref16 [B][16][N_c], eref [B][N_e]."""
+    if loss is None:
+        loss = torch.zeros(1, dtype=torch.float32, device=params.device)
+    arch = _train_arch(fmts, hidden, levels, coarsest)
+    _check(_lib.ntbc_train_endpoint_step(C.byref(arch), params.data_ptr(), grads.data_ptr(), adam_m.data_ptr(),
+                                         adam_v.data_ptr(), step, bxy.data_ptr(), cref16.data_ptr(), eref.data_ptr(),
+                                         bxy.shape[0], blocks_w, blocks_h, temperature, lr_grid, lr_mlp,
+                                         loss.data_ptr(), _stream(stream)))
     return loss
 
 

@@ -75,3 +75,43 @@ def test_train_step_matches_oracle(ntbc, fmts, levels, coarsest, B, temp):
                         torch.zeros(n, dtype=torch.float64), 1, lr)
     got = dp.double().cpu()
     assert torch.allclose(got, want, rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("fmts,levels,coarsest,B,temp", [
+    ([T.BC1, T.BC4], 2, 4, 300, 0.1),
+    ([T.BC1, T.BC1, T.BC4, T.BC4, T.BC4], 7, 16, 1000, 0.01),   # the paper's block grid
+])
+def test_endpoint_train_step_matches_oracle(ntbc, fmts, levels, coarsest, B, temp):
+    rng = np.random.default_rng(B + 7)
+    lay = T.layout_endpoint(fmts, 64, levels, coarsest)
+    n = sum(int(np.prod(s)) for _, s in lay)
+    n_grid = sum(int(np.prod(s)) for nme, s in lay if nme.startswith("grid"))
+    assert ntbc.train_endpoint_param_count(fmts, 64, levels, coarsest) == n
+    p = rng.standard_normal(n) * 0.3
+    p[:n_grid] = rng.uniform(-1, 1, n_grid)
+    p = p.astype(np.float32)
+    n_c = sum(3 if f == T.BC1 else 1 for f in fmts)
+    n_e = sum(6 if f == T.BC1 else 2 for f in fmts)
+    BW, BH = 200, 150
+    bxy = np.stack([rng.integers(0, BW, B), rng.integers(0, BH, B)], 1).astype(np.int32)
+    c16 = rng.uniform(0, 1, (B, 16, n_c)).astype(np.float32)
+    eref = rng.uniform(0, 1, (B, n_e)).astype(np.float32)
+    dp = torch.from_numpy(p).to(DEV)
+    g, m, v = (torch.zeros(n, device=DEV) for _ in range(3))
+    loss = ntbc.train_endpoint_step(fmts, dp, g, m, v, 1, torch.from_numpy(bxy).to(DEV), torch.from_numpy(c16).to(DEV),
+                                    torch.from_numpy(eref).to(DEV), BW, BH, temperature=temp, levels=levels,
+                                    coarsest=coarsest)
+    torch.cuda.synchronize()
+    ref_loss, ref_g, _, _, _ = T.endpoint_step(torch.from_numpy(p.astype(np.float64)), torch.zeros(n, dtype=torch.float64),
+                                               torch.zeros(n, dtype=torch.float64), 1, lay, fmts,
+                                               torch.from_numpy(bxy.astype(np.int64)), BW, BH,
+                                               torch.from_numpy(eref.astype(np.float64)),
+                                               torch.from_numpy(c16.astype(np.float64)), T=temp)
+    assert abs(float(loss) - ref_loss) <= 1e-5 * abs(ref_loss)
+    gg = g.double().cpu()
+    off = 0
+    for name, shape in lay:
+        k = int(np.prod(shape))
+        assert float(torch.linalg.norm(gg[off:off + k] - ref_g[off:off + k])) <= \
+            1e-5 / temp * float(torch.linalg.norm(ref_g)) + 1e-12, name
+        off += k

@@ -153,3 +153,59 @@ def test_adam_matches_torch_optim():
         ref.grad = g.clone()
         opt.step()
         assert torch.allclose(p, ref.detach(), rtol=1e-12, atol=1e-14)
+
+
+def test_endpoint_gradient_vs_finite_differences_of_the_surrogate():
+    """Endpoint network (Eq. 14): the autograd gradient of L_e + L_cd (STE) equals central
+    differences of its first-order surrogate, in which the decoded colour is replaced by the softmax
+    expectation over the REFERENCE palette weighted by 2 (hard - c), the distances taken against the
+    PREDICTED palette."""
+    fmts = [T.BC1, T.BC4]
+    lay = T.layout_endpoint(fmts, 64, 2, 4)
+    n = sum(int(np.prod(s)) for _, s in lay)
+    rng = np.random.default_rng(6)
+    params = torch.from_numpy(rng.standard_normal(n) * 0.3)
+    B, BW, BH, Tt = 6, 16, 12, 2.0
+    bxy = torch.from_numpy(np.stack([rng.integers(0, BW, B), rng.integers(0, BH, B)], 1))
+    eref = torch.from_numpy(rng.uniform(0, 1, (B, 8)))
+    c16 = torch.from_numpy(rng.uniform(0, 1, (B, 16, 4)))
+    x = params.clone().requires_grad_(True)
+    (g,) = torch.autograd.grad(T.endpoint_loss(x, lay, fmts, bxy, BW, BH, eref, c16, Tt), x)
+
+    def ehat_of(p):
+        pp = T.unflatten(p, lay)
+        s = (bxy[:, 0].double() + 0.5) / BW
+        t = (bxy[:, 1].double() + 0.5) / BH
+        a = T.grid_features([pp["grid0"], pp["grid1"]], s, t)
+        for l in range(3):
+            a = torch.nn.functional.selu(a @ pp[f"W{l}"] + pp[f"b{l}"])
+        return torch.sigmoid(a @ pp["W3"] + pp["b3"])
+
+    base = ehat_of(params)
+
+    def surrogate(p):
+        eh = ehat_of(p)
+        loss = ((eh - eref) ** 2).sum()
+        eo = co = 0
+        for f in fmts:
+            w, we = (3, 6) if f == T.BC1 else (1, 2)
+            pp_, pb = T.palettes(f, eh[:, eo:eo + we]), T.palettes(f, base[:, eo:eo + we])
+            pr = T.palettes(f, eref[:, eo:eo + we])
+            for i in range(16):
+                c = c16[:, i, co:co + w]
+                hard = pr[torch.arange(B), torch.argmin(((c[:, None] - pb) ** 2).sum(-1), 1)]
+                d = -torch.sqrt(((c[:, None] - pp_) ** 2).sum(-1))
+                soft = (torch.softmax(d / Tt, 1)[:, :, None] * pr).sum(1)
+                loss = loss + (2 * (hard - c) * soft).sum()
+            eo, co = eo + we, co + w
+        return loss / B
+
+    n_grid = sum(int(np.prod(s)) for nme, s in lay if nme.startswith("grid"))
+    idx = list(rng.choice(n_grid, 8, replace=False)) + list(n_grid + rng.choice(n - n_grid, 24, replace=False))
+    eps = 1e-6
+    for i in idx:
+        pp, pm = params.clone(), params.clone()
+        pp[i] += eps
+        pm[i] -= eps
+        fd = (surrogate(pp) - surrogate(pm)) / (2 * eps)
+        assert abs(float(fd) - float(g[i])) <= 1e-6 + 1e-5 * abs(float(g[i])), (i, float(fd), float(g[i]))

@@ -127,6 +127,7 @@ ntbc_status ntbc_encode_bc(const float* texels, ntbc_format fmt, int width, int 
  *   (atomic accumulation order).  Errors: NTBC_EINVAL, NTBC_ECUDA. */
 typedef struct {
   int n_textures, fmt[8], hidden, levels, coarsest;
+  int qat;   /* 1: the grid passes the per-level 8-bit fake quantizer (Eq. 1-5; DESIGN R33) */
 } ntbc_train_arch;
 long long ntbc_train_param_count(const ntbc_train_arch* arch);   /* floats in the parameter vector; <0: invalid */
 ntbc_status ntbc_train_colour_step(const ntbc_train_arch* arch, float* params, float* grads, float* adam_m,

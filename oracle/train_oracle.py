@@ -4,7 +4,8 @@ Plain PyTorch float64 on the CPU, autograd for the backward pass; only tests/ an
 may import it.  Shares no code with the CUDA path.  One step follows PAPER.md:
 
   * features: the texel grid (fp32 master values, [res][res][2] per level, levels coarse -> fine) sampled
-    at the texel centre exactly as at inference (R1-R3, P:258-272; no QAT: the 90% float phase, P:319);
+    at the texel centre exactly as at inference (R1-R3); optionally through the per-level
+    8-bit fake quantizer of QAT (Eq. 1-5, P:317-324, the last 10% of training);
   * colour MLP 16 -> H -> H -> H -> N_c, selu hidden, sigmoid out (P:331-333), fp32 master weights;
   * loss L_color = L_c + L_cd (Eq. 14-15), per texel and texture:
       L_c  = |c_hat - c|^2,
@@ -49,14 +50,18 @@ def unflatten(vec, lay):
 
 
 def grid_features(grids, u, v):
-    """Vertex-centred bilinear lookup per level (R1), concatenated coarse -> fine (R3)."""
+    """Vertex-centred bilinear lookup per level (R1), concatenated coarse -> fine (R3).  The lattice
+    coordinate is the inference convention (R1, R2): X = RN32(u (res - 1)) with u the binary32 texel
+    centre, fx = X - floor(X) exactly; only the interpolation runs in float64."""
     feats = []
+    u32, v32 = u.to(torch.float32), v.to(torch.float32)
     for g in grids:
         res = g.shape[0]
-        X, Y = u * (res - 1), v * (res - 1)
+        X = u32 * torch.tensor(float(res - 1), dtype=torch.float32)
+        Y = v32 * torch.tensor(float(res - 1), dtype=torch.float32)
         i0 = torch.clamp(torch.floor(X), max=res - 2).long()
         j0 = torch.clamp(torch.floor(Y), max=res - 2).long()
-        fx, fy = (X - i0)[:, None], (Y - j0)[:, None]
+        fx, fy = (X - i0).double()[:, None], (Y - j0).double()[:, None]
         v00, v10 = g[j0, i0], g[j0, i0 + 1]
         v01, v11 = g[j0 + 1, i0], g[j0 + 1, i0 + 1]
         top = v00 + fx * (v10 - v00)
@@ -92,12 +97,51 @@ def ste_decoded(chat, pal, T):
     return soft + (hard - soft).detach()
 
 
-def colour_loss(params, lay, fmts, xy, W, H, cref, eref, T):
+def round_half_away(x):
+    """Eq. 1's half-way rounding, read as round half away from zero (R33), exact in any precision:
+    trunc(x) + sign(x) [|x - trunc(x)| >= 1/2]."""
+    t = torch.trunc(x)
+    return t + torch.sign(x) * (torch.abs(x - t) >= 0.5).to(x.dtype)
+
+
+def qat_params(g):
+    """Per-level asymmetric 8-bit quantizer parameters (Eq. 4-5, R4/R33) in binary32:
+    s = (beta - alpha) / 255 from the level's min/max, z = round(-alpha / s)."""
+    g32 = g.detach().to(torch.float32)
+    alpha, beta = g32.min(), g32.max()
+    s = (beta - alpha) / torch.tensor(255.0, dtype=torch.float32)
+    z = round_half_away(-alpha / s) if float(s) > 0 else torch.zeros((), dtype=torch.float32)
+    return s, z
+
+
+def fake_quant(g):
+    """Q(w) = s (clamp(round(w / s) + z; 0, 255) - z) (Eq. 3) evaluated in binary32 (as the stored
+    int8 codes are dequantized at inference, Eq. 2); STE backward: 1 where not clamped, else 0 (P:174-178,
+    whose printed "w" for the unclamped case is read as 1).  A constant level (s = 0) is left unchanged."""
+    s, z = qat_params(g)
+    if float(s) <= 0:
+        return g
+    g32 = g.detach().to(torch.float32)
+    r = round_half_away(g32 / s) + z
+    q = torch.clamp(r, 0.0, 255.0)
+    mask = (r == q).to(g.dtype)
+    deq = (s * (q - z)).to(g.dtype)
+    return g * mask + (deq - g * mask).detach()
+
+
+def _features(p, lay, levels, u, v, qat):
+    grids = [p[f"grid{l}"] for l in range(levels)]
+    if qat:
+        grids = [fake_quant(g) for g in grids]
+    return grid_features(grids, u, v)
+
+
+def colour_loss(params, lay, fmts, xy, W, H, cref, eref, T, qat=False):
     p = unflatten(params, lay)
     levels = sum(1 for name, _ in lay if name.startswith("grid"))
-    u = (xy[:, 0].double() + 0.5) / W
-    v = (xy[:, 1].double() + 0.5) / H
-    a = grid_features([p[f"grid{l}"] for l in range(levels)], u, v)
+    u = (xy[:, 0].float() + 0.5) / W           # binary32 texel centres (R2)
+    v = (xy[:, 1].float() + 0.5) / H
+    a = _features(p, lay, levels, u, v, qat)
     for l in range(3):
         a = torch.nn.functional.selu(a @ p[f"W{l}"] + p[f"b{l}"])
     chat = torch.sigmoid(a @ p["W3"] + p["b3"])
@@ -122,10 +166,10 @@ def adam(params, grads, m, v, step, lr, beta1=0.9, beta2=0.999, eps=1e-15):
     return params - lr * mh / (torch.sqrt(vh) + eps), m, v
 
 
-def colour_step(params, m, v, step, lay, fmts, xy, W, H, cref, eref, T=0.01, lr_grid=0.01, lr_mlp=0.005):
+def colour_step(params, m, v, step, lay, fmts, xy, W, H, cref, eref, T=0.01, lr_grid=0.01, lr_mlp=0.005, qat=False):
     """One training step; all arrays float64 torch tensors (xy int).  Returns (loss, grads, params, m, v)."""
     x = params.clone().requires_grad_(True)
-    loss = colour_loss(x, lay, fmts, xy, W, H, cref, eref, T)
+    loss = colour_loss(x, lay, fmts, xy, W, H, cref, eref, T, qat)
     (g,) = torch.autograd.grad(loss, x)
     n_grid = sum(int(np.prod(s)) for name, s in lay if name.startswith("grid"))
     lr = torch.full_like(params, lr_mlp)
@@ -145,16 +189,16 @@ def layout_endpoint(fmts, hidden, levels, coarsest):
     return out
 
 
-def endpoint_loss(params, lay, fmts, bxy, BW, BH, eref, cref16, T):
+def endpoint_loss(params, lay, fmts, bxy, BW, BH, eref, cref16, T, qat=False):
     """L_endpoint = L_e + L_cd (Eq. 14), batch mean.  eref [B][N_e] reference endpoints, cref16
     [B][16][N_c] reference colours of the block's texels (texel i = 4y + x).  The index of each texel
     comes from the PREDICTED endpoints' palette and the reference colour; the decoded colour is the
     REFERENCE endpoints' palette entry at that index; STE as for the colour network."""
     p = unflatten(params, lay)
     levels = sum(1 for name, _ in lay if name.startswith("grid"))
-    s = (bxy[:, 0].double() + 0.5) / BW
-    t = (bxy[:, 1].double() + 0.5) / BH
-    a = grid_features([p[f"grid{l}"] for l in range(levels)], s, t)
+    s = (bxy[:, 0].float() + 0.5) / BW         # binary32 block centres (R2)
+    t = (bxy[:, 1].float() + 0.5) / BH
+    a = _features(p, lay, levels, s, t, qat)
     for l in range(3):
         a = torch.nn.functional.selu(a @ p[f"W{l}"] + p[f"b{l}"])
     ehat = torch.sigmoid(a @ p["W3"] + p["b3"])
@@ -179,12 +223,65 @@ def endpoint_loss(params, lay, fmts, bxy, BW, BH, eref, cref16, T):
     return loss / B
 
 
-def endpoint_step(params, m, v, step, lay, fmts, bxy, BW, BH, eref, cref16, T=0.01, lr_grid=0.01, lr_mlp=0.005):
+def endpoint_step(params, m, v, step, lay, fmts, bxy, BW, BH, eref, cref16, T=0.01, lr_grid=0.01, lr_mlp=0.005,
+                  qat=False):
     x = params.clone().requires_grad_(True)
-    loss = endpoint_loss(x, lay, fmts, bxy, BW, BH, eref, cref16, T)
+    loss = endpoint_loss(x, lay, fmts, bxy, BW, BH, eref, cref16, T, qat)
     (g,) = torch.autograd.grad(loss, x)
     n_grid = sum(int(np.prod(s)) for name, s in lay if name.startswith("grid"))
     lr = torch.full_like(params, lr_mlp)
     lr[:n_grid] = lr_grid
     p2, m2, v2 = adam(params, g, m, v, step, lr)
     return float(loss.detach()), g, p2, m2, v2
+
+
+# ---------------------------------------------------------------- test support: argmax decision margins
+def _margin(dist):
+    s, _ = torch.sort(dist, dim=1)
+    return s[:, 1] - s[:, 0]
+
+
+@torch.no_grad()
+def colour_margins(params, lay, fmts, xy, W, H, eref, qat=False):
+    """Per sample: the smallest gap between the nearest and second-nearest palette distance over the
+    textures (float64).  Samples with a tiny gap can take the other argmax branch in fp32 arithmetic;
+    parity tests drop them (the decision itself is discrete)."""
+    p = unflatten(params, lay)
+    levels = sum(1 for name, _ in lay if name.startswith("grid"))
+    u = (xy[:, 0].float() + 0.5) / W           # binary32 texel centres (R2)
+    v = (xy[:, 1].float() + 0.5) / H
+    a = _features(p, lay, levels, u, v, qat)
+    for l in range(3):
+        a = torch.nn.functional.selu(a @ p[f"W{l}"] + p[f"b{l}"])
+    chat = torch.sigmoid(a @ p["W3"] + p["b3"])
+    m = torch.full((xy.shape[0],), float("inf"), dtype=torch.float64)
+    co = eo = 0
+    for f in fmts:
+        w, we = (3, 6) if f == BC1 else (1, 2)
+        pal = palettes(f, eref[:, eo:eo + we])
+        dist = torch.sqrt(((chat[:, co:co + w][:, None] - pal) ** 2).sum(-1))
+        m = torch.minimum(m, _margin(dist))
+        co, eo = co + w, eo + we
+    return m
+
+
+@torch.no_grad()
+def endpoint_margins(params, lay, fmts, bxy, BW, BH, cref16, qat=False):
+    p = unflatten(params, lay)
+    levels = sum(1 for name, _ in lay if name.startswith("grid"))
+    s = (bxy[:, 0].float() + 0.5) / BW         # binary32 block centres (R2)
+    t = (bxy[:, 1].float() + 0.5) / BH
+    a = _features(p, lay, levels, s, t, qat)
+    for l in range(3):
+        a = torch.nn.functional.selu(a @ p[f"W{l}"] + p[f"b{l}"])
+    ehat = torch.sigmoid(a @ p["W3"] + p["b3"])
+    m = torch.full((bxy.shape[0],), float("inf"), dtype=torch.float64)
+    eo = co = 0
+    for f in fmts:
+        w, we = (3, 6) if f == BC1 else (1, 2)
+        pal = palettes(f, ehat[:, eo:eo + we])
+        for i in range(16):
+            dist = torch.sqrt(((cref16[:, i, co:co + w][:, None] - pal) ** 2).sum(-1))
+            m = torch.minimum(m, _margin(dist))
+        eo, co = eo + we, co + w
+    return m

@@ -683,6 +683,24 @@ ntbc_status train_step(int net, const ntbc_train_arch* arch, float* params, floa
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaMemsetAsync(grads, 0, (size_t)n * sizeof(float), st));
   CUDA_TRY(cudaMemsetAsync(loss, 0, sizeof(float), st));
+  p.qsz = nullptr;
+  if (arch->qat) {   // QAT: per-level min/max -> (s, z) of the 8-bit fake quantizer, on the GPU
+    static thread_local int* d_q = nullptr;   // [2*kMaxLevels] ordered-int min/max, then [2*kMaxLevels] (s, z)
+    if (!d_q && cudaMalloc(&d_q, 4 * kMaxLevels * sizeof(int)) != cudaSuccess) { cudaGetLastError(); d_q = nullptr; return fail(NTBC_ENOMEM, "QAT scratch"); }
+    int init[2 * kMaxLevels];
+    for (int l = 0; l < kMaxLevels; l++) { init[2 * l] = 0x7FFFFFFF; init[2 * l + 1] = (int)0x80000000; }
+    CUDA_TRY(cudaMemcpyAsync(d_q, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    LevelList L{};
+    for (int l = 0; l < p.levels; l++) {
+      const long long res = (long long)p.coarsest << l;
+      L.off[l] = p.lvl_off[l];
+      L.cnt[l] = res * res * 2;
+    }
+    level_minmax_kernel<<<dim3(148, p.levels), 256, 0, st>>>(params, L, p.levels, d_q);
+    qat_params_kernel<<<1, 32, 0, st>>>(d_q, p.levels, reinterpret_cast<float*>(d_q + 2 * kMaxLevels));
+    g_launches += 2;
+    p.qsz = reinterpret_cast<const float*>(d_q + 2 * kMaxLevels);
+  }
   p.params = params; p.grads = grads; p.xy = xy; p.cref = cref; p.eref = eref;
   p.B = batch; p.W = width; p.H = height; p.T = temperature; p.loss = loss;
   size_t smem = 0;

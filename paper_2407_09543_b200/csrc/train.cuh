@@ -33,7 +33,54 @@ struct TrainParams {
   int B, W, H;
   float T;
   float* loss;                        // += batch-mean loss
+  const float* qsz;                   // QAT: per level (s, z) of the 8-bit fake quantizer, or nullptr
 };
+
+// Eq. 1/3 rounding, read as half away from zero (R33): roundf
+// QAT fake quantizer (Eq. 3) of one grid value in binary32; `pass` = 1 where not clamped (STE)
+__device__ __forceinline__ float fake_quant(float w, const float* qsz, int l, float& pass) {
+  pass = 1.0f;
+  if (!qsz) return w;
+  const float s = qsz[2 * l], z = qsz[2 * l + 1];
+  if (!(s > 0.0f)) return w;
+  const float r = roundf(__fdiv_rn(w, s)) + z;
+  const float q = fminf(fmaxf(r, 0.0f), 255.0f);
+  pass = r == q ? 1.0f : 0.0f;
+  return s * (q - z);
+}
+
+// per-level min / max of the grid (QAT ranges, Eq. 4): ordered-int atomics on [2*levels] slots
+__device__ __forceinline__ int f2ord(float f) { const int i = __float_as_int(f); return i >= 0 ? i : i ^ 0x7FFFFFFF; }
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+struct LevelList { long long off[kMaxLevels], cnt[kMaxLevels]; };
+__global__ void __launch_bounds__(256) level_minmax_kernel(const float* __restrict__ params, const LevelList L,
+                                                           int levels, int* __restrict__ mm) {
+  const int l = blockIdx.y;
+  if (l >= levels) return;
+  int lo = 0x7FFFFFFF, hi = (int)0x80000000;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L.cnt[l]; i += (long long)gridDim.x * blockDim.x) {
+    const int o = f2ord(params[L.off[l] + i]);
+    lo = min(lo, o);
+    hi = max(hi, o);
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, d));
+    hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, d));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm + 2 * l, lo);
+    atomicMax(mm + 2 * l + 1, hi);
+  }
+}
+// s = (beta - alpha) / 255, z = round(-alpha / s) (Eq. 4-5, R4, R33), in binary32
+__global__ void qat_params_kernel(const int* __restrict__ mm, int levels, float* __restrict__ qsz) {
+  const int l = threadIdx.x;
+  if (l >= levels) return;
+  const float alpha = ord2f(mm[2 * l]), beta = ord2f(mm[2 * l + 1]);
+  const float s = __fdiv_rn(beta - alpha, 255.0f);
+  qsz[2 * l] = s;
+  qsz[2 * l + 1] = s > 0.0f ? roundf(__fdiv_rn(-alpha, s)) : 0.0f;
+}
 
 __device__ __forceinline__ float selu_f(float z) { return z > 0.0f ? kSeluL * z : kSeluLA * (expf(z) - 1.0f); }
 
@@ -102,8 +149,11 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_
     const float fx = X - (float)i0, fy = Y - (float)j0;
     const float* g = p.params + p.lvl_off[l];
     for (int f = 0; f < 2; f++) {
-      const float v00 = g[((size_t)j0 * res + i0) * 2 + f], v10 = g[((size_t)j0 * res + i0 + 1) * 2 + f];
-      const float v01 = g[((size_t)(j0 + 1) * res + i0) * 2 + f], v11 = g[((size_t)(j0 + 1) * res + i0 + 1) * 2 + f];
+      float pass;
+      const float v00 = fake_quant(g[((size_t)j0 * res + i0) * 2 + f], p.qsz, l, pass);
+      const float v10 = fake_quant(g[((size_t)j0 * res + i0 + 1) * 2 + f], p.qsz, l, pass);
+      const float v01 = fake_quant(g[((size_t)(j0 + 1) * res + i0) * 2 + f], p.qsz, l, pass);
+      const float v11 = fake_quant(g[((size_t)(j0 + 1) * res + i0 + 1) * 2 + f], p.qsz, l, pass);
       const float top = v00 + fx * (v10 - v00), bot = v01 + fx * (v11 - v01);
       A[0][tid * ldA[0] + 2 * l + f] = top + fy * (bot - top);
     }
@@ -282,12 +332,19 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_
       const int i0 = min((int)floorf(X), res - 2), j0 = min((int)floorf(Y), res - 2);
       const float fx = X - (float)i0, fy = Y - (float)j0;
       float* g = p.grads + p.lvl_off[l];
+      const float* gv = p.params + p.lvl_off[l];
+      const size_t c00 = ((size_t)j0 * res + i0) * 2, c10 = c00 + 2, c01 = c00 + (size_t)res * 2, c11 = c01 + 2;
       for (int f = 0; f < 2; f++) {
         const float d = D[tid * LD + 2 * l + f];
-        atomicAdd(g + ((size_t)j0 * res + i0) * 2 + f, d * (1.0f - fx) * (1.0f - fy));
-        atomicAdd(g + ((size_t)j0 * res + i0 + 1) * 2 + f, d * fx * (1.0f - fy));
-        atomicAdd(g + ((size_t)(j0 + 1) * res + i0) * 2 + f, d * (1.0f - fx) * fy);
-        atomicAdd(g + ((size_t)(j0 + 1) * res + i0 + 1) * 2 + f, d * fx * fy);
+        float m00, m10, m01, m11;   // QAT STE: no gradient through clamped values
+        fake_quant(gv[c00 + f], p.qsz, l, m00);
+        fake_quant(gv[c10 + f], p.qsz, l, m10);
+        fake_quant(gv[c01 + f], p.qsz, l, m01);
+        fake_quant(gv[c11 + f], p.qsz, l, m11);
+        atomicAdd(g + c00 + f, m00 * d * (1.0f - fx) * (1.0f - fy));
+        atomicAdd(g + c10 + f, m10 * d * fx * (1.0f - fy));
+        atomicAdd(g + c01 + f, m01 * d * (1.0f - fx) * fy);
+        atomicAdd(g + c11 + f, m11 * d * fx * fy);
       }
     }
   }

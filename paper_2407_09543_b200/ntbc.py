@@ -160,11 +160,12 @@ def encode_bc(texels: torch.Tensor, fmt: int, width: int, height: int, n_refine:
 
 class _TrainArch(C.Structure):
     _fields_ = [("n_textures", C.c_int), ("fmt", C.c_int * 8), ("hidden", C.c_int), ("levels", C.c_int),
-                ("coarsest", C.c_int)]
+                ("coarsest", C.c_int), ("qat", C.c_int)]
 
 
-def _train_arch(fmts, hidden, levels, coarsest):
+def _train_arch(fmts, hidden, levels, coarsest, qat=False):
     a = _TrainArch()
+    a.qat = int(bool(qat))
     a.n_textures = len(fmts)
     for i, f in enumerate(fmts):
         a.fmt[i] = f
@@ -181,11 +182,11 @@ def train_param_count(fmts, hidden=64, levels=8, coarsest=16) -> int:
 
 def train_colour_step(fmts, params, grads, adam_m, adam_v, step, xy, cref, eref, width, height,
                       temperature=0.01, lr_grid=0.01, lr_mlp=0.005, hidden=64, levels=8, coarsest=16,
-                      loss=None, stream=None):
+                      loss=None, stream=None, qat=False):
     """ntbc_train_colour_step on device fp32 tensors (params/grads/adam_m/adam_v: flat; xy int32 [B][2])."""
     if loss is None:
         loss = torch.zeros(1, dtype=torch.float32, device=params.device)
-    arch = _train_arch(fmts, hidden, levels, coarsest)
+    arch = _train_arch(fmts, hidden, levels, coarsest, qat)
     _check(_lib.ntbc_train_colour_step(C.byref(arch), params.data_ptr(), grads.data_ptr(), adam_m.data_ptr(),
                                        adam_v.data_ptr(), step, xy.data_ptr(), cref.data_ptr(), eref.data_ptr(),
                                        xy.shape[0], width, height, temperature, lr_grid, lr_mlp, loss.data_ptr(),
@@ -202,11 +203,11 @@ def train_endpoint_param_count(fmts, hidden=64, levels=7, coarsest=16) -> int:
 
 def train_endpoint_step(fmts, params, grads, adam_m, adam_v, step, bxy, cref16, eref, blocks_w, blocks_h,
                         temperature=0.01, lr_grid=0.01, lr_mlp=0.005, hidden=64, levels=7, coarsest=16,
-                        loss=None, stream=None):
+                        loss=None, stream=None, qat=False):
     """ntbc_train_endpoint_step: bxy int32 [B][2] block coords, cref16 [B][16][N_c], eref [B][N_e]."""
     if loss is None:
         loss = torch.zeros(1, dtype=torch.float32, device=params.device)
-    arch = _train_arch(fmts, hidden, levels, coarsest)
+    arch = _train_arch(fmts, hidden, levels, coarsest, qat)
     _check(_lib.ntbc_train_endpoint_step(C.byref(arch), params.data_ptr(), grads.data_ptr(), adam_m.data_ptr(),
                                          adam_v.data_ptr(), step, bxy.data_ptr(), cref16.data_ptr(), eref.data_ptr(),
                                          bxy.shape[0], blocks_w, blocks_h, temperature, lr_grid, lr_mlp,

@@ -20,13 +20,16 @@ def _setup(fmts, levels=2, coarsest=4, B=64, seed=0, W=32, H=32):
 
 
 def test_grid_features_vs_torch_grid_sample():
-    """The vertex-centred lookup (R1) is grid_sample with align_corners=True at the same point."""
+    """The vertex-centred lookup (R1) is grid_sample with align_corners=True at the same lattice point
+    (X = RN32(u (res-1)), the inference convention, passed to grid_sample as its normalized coordinate)."""
     rng = np.random.default_rng(1)
     g = torch.from_numpy(rng.standard_normal((9, 9, 2)))
-    u = torch.from_numpy(rng.uniform(0.01, 0.99, 100))
-    v = torch.from_numpy(rng.uniform(0.01, 0.99, 100))
+    u = torch.from_numpy(rng.uniform(0.01, 0.99, 100).astype(np.float32))
+    v = torch.from_numpy(rng.uniform(0.01, 0.99, 100).astype(np.float32))
     ours = T.grid_features([g], u, v)
-    ref = torch.nn.functional.grid_sample(g.permute(2, 0, 1)[None], torch.stack([2 * u - 1, 2 * v - 1], 1)[None, None],
+    X = (u * torch.tensor(8.0, dtype=torch.float32)).double()
+    Y = (v * torch.tensor(8.0, dtype=torch.float32)).double()
+    ref = torch.nn.functional.grid_sample(g.permute(2, 0, 1)[None], torch.stack([X / 4 - 1, Y / 4 - 1], 1)[None, None],
                                           mode="bilinear", align_corners=True)[0, :, 0].T
     assert torch.allclose(ours, ref, atol=1e-12)
 
@@ -106,8 +109,8 @@ def test_full_gradient_vs_finite_differences_of_the_surrogate():
     def surrogate(p):
         # first-order model of the STE loss around the current hard decisions
         pp = T.unflatten(p, lay)
-        u = (xy[:, 0].double() + 0.5) / W
-        v = (xy[:, 1].double() + 0.5) / H
+        u = (xy[:, 0].float() + 0.5) / W
+        v = (xy[:, 1].float() + 0.5) / H
         a = T.grid_features([pp[f"grid{l}"] for l in range(2)], u, v)
         for l in range(3):
             a = torch.nn.functional.selu(a @ pp[f"W{l}"] + pp[f"b{l}"])
@@ -174,8 +177,8 @@ def test_endpoint_gradient_vs_finite_differences_of_the_surrogate():
 
     def ehat_of(p):
         pp = T.unflatten(p, lay)
-        s = (bxy[:, 0].double() + 0.5) / BW
-        t = (bxy[:, 1].double() + 0.5) / BH
+        s = (bxy[:, 0].float() + 0.5) / BW
+        t = (bxy[:, 1].float() + 0.5) / BH
         a = T.grid_features([pp["grid0"], pp["grid1"]], s, t)
         for l in range(3):
             a = torch.nn.functional.selu(a @ pp[f"W{l}"] + pp[f"b{l}"])
@@ -209,3 +212,27 @@ def test_endpoint_gradient_vs_finite_differences_of_the_surrogate():
         pm[i] -= eps
         fd = (surrogate(pp) - surrogate(pm)) / (2 * eps)
         assert abs(float(fd) - float(g[i])) <= 1e-6 + 1e-5 * abs(float(g[i])), (i, float(fd), float(g[i]))
+
+
+def test_qat_fake_quant_equals_inference_dequantization():
+    """QAT (Eq. 1-5): the fake-quantized grid value is exactly what inference computes from the
+    stored code (Eq. 2, the C oracle's o_dequant), the rounding error is at most s/2 inside the range,
+    and the STE passes the gradient (1) only where the code is not clamped."""
+    import oracle as O
+    rng = np.random.default_rng(8)
+    for lo, hi in ((-0.3, 0.7), (0.1, 0.2), (-1e-4, 1e-4)):
+        g = torch.from_numpy(rng.uniform(lo, hi, (12, 12, 2))).requires_grad_(True)
+        s, z = T.qat_params(g)
+        q_val = T.fake_quant(g)
+        r = T.round_half_away(g.detach().float() / s) + z
+        codes = torch.clamp(r, 0, 255)
+        deq = np.array([O.lib().o_dequant(int(c), float(s), int(z)) for c in codes.reshape(-1).tolist()], np.float32)
+        assert np.array_equal(q_val.detach().float().reshape(-1).numpy(), deq)
+        inside = (r == codes).reshape(-1).numpy()
+        err = np.abs(q_val.detach().numpy().reshape(-1) - g.detach().numpy().reshape(-1))
+        assert np.all(err[inside] <= float(s) * 0.5 * (1 + 1e-5) + 1e-12)
+        (grad,) = torch.autograd.grad(q_val.sum(), g)
+        assert np.array_equal(grad.reshape(-1).numpy(), inside.astype(np.float64))
+    # half-way rounding: away from zero, exactly (the float32 floor(|x| + 1/2) shortcut fails at 0.49999997)
+    x = torch.tensor([0.5, -0.5, 1.5, -2.5, 0.49999997, -0.49999997], dtype=torch.float32)
+    assert T.round_half_away(x).tolist() == [1.0, -1.0, 2.0, -3.0, 0.0, -0.0]

@@ -233,7 +233,6 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
     CUDA_TRY(cudaMemsetAsync(p.next_unit, 0, sizeof(int), st));
   }
   p.blob = m->d_blob;
-  p.k23 = 1 << 23;
   for (int g = 0; g < 2; g++) {
     p.levels[g] = a.levels[g];
     for (int l = 0; l < a.levels[g]; l++) {

@@ -49,7 +49,6 @@ struct FusedParams {
   float* dump_col;  // DUMP mode: [rows*4][W][N_c]
   uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
   uint32_t debug_flags;         // bit 1: grid-feature dump (ntbc_debug_features)
-  int k23;                      // = 1 << 23 (run-time constant, see selu2_h2)
   unsigned long long* progress; // optional: per-chunk count of finished units (pipelined D2H, see ntbc_api.cu)
   int chunk_rows;               // block rows per progress chunk
   int* next_unit;               // optional: dynamic unit counter (zeroed before the launch)
@@ -254,7 +253,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           uint32_t hv[8];
 #pragma unroll
           for (int j = 0; j < 8; j++)
-            hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]), p.k23);
+            hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
           *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
           *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
           if (PF && c + 1 < H / 16) tmem_wait_ld16(buf[(c + 1) & 1]);

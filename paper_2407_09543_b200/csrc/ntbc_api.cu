@@ -712,7 +712,7 @@ ntbc_status train_step(int net, const ntbc_train_arch* arch, float* params, floa
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured[net] = true;
   }
-  kern<<<(batch + kTrainTile - 1) / kTrainTile, kTrainTile, smem, st>>>(p);
+  kern<<<(batch + kTrainTile - 1) / kTrainTile, kTrainTile * kTrainQ, smem, st>>>(p);
   g_launches++;
   const double bc1 = 1.0 - std::pow(0.9, step), bc2 = 1.0 - std::pow(0.999, step);
   const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 32);

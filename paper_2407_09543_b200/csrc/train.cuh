@@ -5,19 +5,23 @@
 // with separate grid / MLP learning rates.  DESIGN.md R30-R32 fix the parameter layout,
 // the batch-mean loss and this implementation's precision (fp32 throughout, CUDA cores).
 //
-// Kernel (1) train_colour_kernel: one CTA = 128 texel samples, one thread per sample.  The MLP
+// Kernel (1) train_step_kernel: one CTA = 128 samples, four threads per sample (each owns a quarter of
+// every layer's outputs and inputs).  The MLP
 // weights live in shared memory; the layer inputs of the tile (features, three hidden activations)
 // are kept in shared memory for the backward pass (selu' is recovered from the activation:
 // lambda for a > 0, a + lambda*alpha otherwise).  Weight gradients are reduced over the tile in
 // shared memory and added to the global gradient with one atomic per weight per CTA; the grid
 // gradient is scattered with atomics (4 vertices x 2 features per level per sample).
 // Kernel (2) adam_kernel: bias-corrected Adam over the flat parameter vector.
+// The library is compiled with --fmad=false (bit-exact inference); the training loops use explicit
+// __fmaf_rn so their dot products still run as FFMA.
 #pragma once
 #include <cstdint>
 
 namespace ntbc {
 
 constexpr int kTrainTile = 128;
+constexpr int kTrainQ = 4;     // threads per sample
 constexpr float kSeluL = 1.0507009873554804934f, kSeluLA = 1.0507009873554804934f * 1.6732632423543772848f;
 
 struct TrainParams {
@@ -114,9 +118,12 @@ __device__ __forceinline__ float train_weight(int fmt, bool mode8, int n, bool& 
 
 // NET = 1: colour network (samples are texels); NET = 0: endpoint network (samples are blocks)
 template <int HID, int NET>
-__global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_constant__ TrainParams p) {
+__global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(const __grid_constant__ TrainParams p) {
   extern __shared__ float sm[];
-  const int tid = threadIdx.x, n_c = NET ? p.n_c : p.n_e, F = 2 * p.levels;   // n_c here = MLP outputs
+  // kTrainQ threads per sample: thread (tid, h) owns sample tid of the tile and the h-th quarter of each
+  // layer's outputs / inputs (more warps per SM at the same shared memory)
+  const int t = threadIdx.x, tid = t % kTrainTile, h = t / kTrainTile, NT = kTrainTile * kTrainQ;
+  const int n_c = NET ? p.n_c : p.n_e, F = 2 * p.levels;   // n_c here = MLP outputs
   constexpr int LD = HID + 1;                                   // padded row stride (bank-conflict free)
   // ---- shared memory: weights, biases, tile activations A0 (features), A1..A3, delta buffer
   float* sW[4];
@@ -131,8 +138,8 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_
   const int ldA[4] = {F + 1, LD, LD, LD};
   for (int l = 0; l < 4; l++) {
     const int nw = p.kin[l] * p.kout[l];
-    for (int t = tid; t < nw; t += kTrainTile) sW[l][t] = p.params[p.w_off[l] + t];
-    for (int t = tid; t < p.kout[l]; t += kTrainTile) sb[l][t] = p.params[p.b_off[l] + t];
+    for (int e = t; e < nw; e += NT) sW[l][e] = p.params[p.w_off[l] + e];
+    for (int e = t; e < p.kout[l]; e += NT) sb[l][e] = p.params[p.b_off[l] + e];
   }
   __syncthreads();
 
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_
   const float u = ((float)p.xy[2 * sc] + 0.5f) / (float)p.W, v = ((float)p.xy[2 * sc + 1] + 0.5f) / (float)p.H;
 
   // ---- forward: grid features (R1-R3), hidden layers, sigmoid outputs
-  for (int l = 0; l < p.levels; l++) {
+  for (int l = h; l < p.levels; l += kTrainQ) {
     const int res = p.coarsest << l;
     const float X = u * (float)(res - 1), Y = v * (float)(res - 1);
     const int i0 = min((int)floorf(X), res - 2), j0 = min((int)floorf(Y), res - 2);
@@ -158,150 +165,158 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_
       A[0][tid * ldA[0] + 2 * l + f] = top + fy * (bot - top);
     }
   }
+  __syncthreads();
+  constexpr int HQ = HID / kTrainQ;
   for (int l = 0; l < 3; l++) {
     const float* a = A[l] + tid * ldA[l];
     float* o = A[l + 1] + tid * LD;
-    for (int j = 0; j < HID; j++) {
+    for (int j = h * HQ; j < (h + 1) * HQ; j++) {
       float z = sb[l][j];
-      for (int k = 0; k < p.kin[l]; k++) z += a[k] * sW[l][k * HID + j];
+      for (int k = 0; k < p.kin[l]; k++) z = __fmaf_rn(a[k], sW[l][k * HID + j], z);
       o[j] = selu_f(z);
     }
+    __syncthreads();
   }
-  float chat[6 * kMaxTex], g_out[6 * kMaxTex];
-  {
+  float* D = Dl;
+  {   // output layer: column j by quarter j % kTrainQ, staged through D
     const float* a = A[3] + tid * LD;
-    for (int j = 0; j < n_c; j++) {
+    for (int j = h; j < n_c; j += kTrainQ) {
       float z = sb[3][j];
-      for (int k = 0; k < HID; k++) z += a[k] * sW[3][k * n_c + j];
-      chat[j] = 1.0f / (1.0f + expf(-z));
+      for (int k = 0; k < HID; k++) z = __fmaf_rn(a[k], sW[3][k * n_c + j], z);
+      D[tid * LD + j] = 1.0f / (1.0f + expf(-z));
     }
   }
+  __syncthreads();
+  float chat[6 * kMaxTex], g_out[6 * kMaxTex];
+  for (int j = 0; j < n_c; j++) chat[j] = D[tid * LD + j];
 
+  if (h == 0) {
   if constexpr (NET == 1) {
-    // ---- loss and dL/dc_hat per texture: L_c + L_cd with the STE expectation (App. A)
-    float loss = 0.0f;
-    {
-      int co = 0, eo = 0;
-      const float invB = 1.0f / (float)p.B, invT = 1.0f / p.T;
-      for (int k = 0; k < p.n_tex; k++) {
-        const int w = p.fmt[k] == kFmtBC1 ? 3 : 1;
-        float pal[24], e[6], c[3], ch[3];
-        for (int t = 0; t < 2 * w; t++) e[t] = p.eref[(size_t)sc * p.n_e + eo + t];
-        for (int t = 0; t < w; t++) { c[t] = p.cref[(size_t)sc * n_c + co + t]; ch[t] = chat[co + t]; }
-        const int nn = train_palette(p.fmt[k], e, pal);
-        float dist[8], dmax = -1e30f;
-        int best = 0;
-        for (int n = 0; n < nn; n++) {
-          float s2 = 0.0f;
-          for (int t = 0; t < w; t++) { const float d = ch[t] - pal[n * w + t]; s2 += d * d; }
-          dist[n] = sqrtf(fmaxf(s2, 1e-30f));
-          if (-dist[n] > dmax) { dmax = -dist[n]; best = n; }        // argmax of d_n = -dist, ties -> lower n
-        }
-        float sig[8], ssum = 0.0f;
-        for (int n = 0; n < nn; n++) { sig[n] = expf((-dist[n] - dmax) * invT); ssum += sig[n]; }
-        for (int n = 0; n < nn; n++) sig[n] /= ssum;
-        // forward values: L_c = |c_hat - c|^2, L_cd = |c_n(best) - c|^2
-        float G[8], gd[3];
-        for (int t = 0; t < w; t++) {
-          const float dc = ch[t] - c[t], dd = pal[best * w + t] - c[t];
-          loss += dc * dc + dd * dd;
-          gd[t] = 2.0f * dd;                                         // dL/dc_dec (forward value)
-        }
-        float sG = 0.0f;
-        for (int n = 0; n < nn; n++) {                               // G_n = dL/dc_dec . c_n
-          G[n] = 0.0f;
-          for (int t = 0; t < w; t++) G[n] += gd[t] * pal[n * w + t];
-          sG += sig[n] * G[n];
-        }
-        for (int x = 0; x < w; x++) {
-          // d soft / d c_hat_x = (1/T) sum_n sigma_n (G_n - sum_m sigma_m G_m) dd_n/dc_hat_x,
-          // dd_n / dc_hat_x = -(c_hat_x - c_n,x) / dist_n
-          float acc = 0.0f;
-          for (int n = 0; n < nn; n++) acc += sig[n] * (G[n] - sG) * (-(ch[x] - pal[n * w + x]) / dist[n]);
-          const float gx = 2.0f * (ch[x] - c[x]) + invT * acc;
-          g_out[co + x] = valid ? gx * invB * ch[x] * (1.0f - ch[x]) : 0.0f;   // through the sigmoid
-        }
-        co += w;
-        eo += 2 * w;
-      }
-    }
-  red[tid] = valid ? loss : 0.0f;
-  } else {
-  // ---- endpoint network: L_e + L_cd (Eq. 14); indices from the PREDICTED palette and the reference
-    //      colours, decoded colour from the REFERENCE palette, STE as for the colour net
-    float loss = 0.0f;
-    {
-      const float invB = 1.0f / (float)p.B, invT = 1.0f / p.T;
-      for (int j = 0; j < n_c; j++) {
-        const float d = chat[j] - p.eref[(size_t)sc * n_c + j];
-        loss += d * d;
-        g_out[j] = 2.0f * d;
-      }
-      int co = 0, eo = 0;
-      for (int k = 0; k < p.n_tex; k++) {
-        const int w = p.fmt[k] == kFmtBC1 ? 3 : 1;
-        float pp[24], pr[24], ep[6], er[6];
-        for (int t = 0; t < 2 * w; t++) { ep[t] = chat[eo + t]; er[t] = p.eref[(size_t)sc * n_c + eo + t]; }
-        const int nn = train_palette(p.fmt[k], ep, pp);
-        train_palette(p.fmt[k], er, pr);
-        const bool mode8 = p.fmt[k] == kFmtBC1 || ep[0] > ep[1];
-        for (int i = 0; i < 16; i++) {
-          float c[3];
-          for (int t = 0; t < w; t++) c[t] = p.cref[((size_t)sc * 16 + i) * p.n_c + co + t];
+      // ---- loss and dL/dc_hat per texture: L_c + L_cd with the STE expectation (App. A)
+      float loss = 0.0f;
+      {
+        int co = 0, eo = 0;
+        const float invB = 1.0f / (float)p.B, invT = 1.0f / p.T;
+        for (int k = 0; k < p.n_tex; k++) {
+          const int w = p.fmt[k] == kFmtBC1 ? 3 : 1;
+          float pal[24], e[6], c[3], ch[3];
+          for (int t = 0; t < 2 * w; t++) e[t] = p.eref[(size_t)sc * p.n_e + eo + t];
+          for (int t = 0; t < w; t++) { c[t] = p.cref[(size_t)sc * n_c + co + t]; ch[t] = chat[co + t]; }
+          const int nn = train_palette(p.fmt[k], e, pal);
           float dist[8], dmax = -1e30f;
           int best = 0;
           for (int n = 0; n < nn; n++) {
             float s2 = 0.0f;
-            for (int t = 0; t < w; t++) { const float d = c[t] - pp[n * w + t]; s2 += d * d; }
+            for (int t = 0; t < w; t++) { const float d = ch[t] - pal[n * w + t]; s2 += d * d; }
             dist[n] = sqrtf(fmaxf(s2, 1e-30f));
-            if (-dist[n] > dmax) { dmax = -dist[n]; best = n; }
+            if (-dist[n] > dmax) { dmax = -dist[n]; best = n; }        // argmax of d_n = -dist, ties -> lower n
           }
           float sig[8], ssum = 0.0f;
           for (int n = 0; n < nn; n++) { sig[n] = expf((-dist[n] - dmax) * invT); ssum += sig[n]; }
           for (int n = 0; n < nn; n++) sig[n] /= ssum;
-          float gd[3], G[8], sG = 0.0f;
+          // forward values: L_c = |c_hat - c|^2, L_cd = |c_n(best) - c|^2
+          float G[8], gd[3];
           for (int t = 0; t < w; t++) {
-            const float dd = pr[best * w + t] - c[t];
-            loss += dd * dd;
-            gd[t] = 2.0f * dd;
+            const float dc = ch[t] - c[t], dd = pal[best * w + t] - c[t];
+            loss += dc * dc + dd * dd;
+            gd[t] = 2.0f * dd;                                         // dL/dc_dec (forward value)
           }
-          for (int n = 0; n < nn; n++) {
+          float sG = 0.0f;
+          for (int n = 0; n < nn; n++) {                               // G_n = dL/dc_dec . c_n
             G[n] = 0.0f;
-            for (int t = 0; t < w; t++) G[n] += gd[t] * pr[n * w + t];
+            for (int t = 0; t < w; t++) G[n] += gd[t] * pal[n * w + t];
             sG += sig[n] * G[n];
           }
-          for (int n = 0; n < nn; n++) {
-            bool constant;
-            const float wn = train_weight(p.fmt[k], mode8, n, constant);
-            if (constant) continue;
-            const float coef = invT * sig[n] * (G[n] - sG);        // dL/dd_n
-            for (int x = 0; x < w; x++) {
-              const float dpal = coef * (-(pp[n * w + x] - c[x]) / dist[n]);   // dL/d pal_pred[n][x]
-              g_out[eo + x] += dpal * (1.0f - wn);
-              g_out[eo + w + x] += dpal * wn;
+          for (int x = 0; x < w; x++) {
+            // d soft / d c_hat_x = (1/T) sum_n sigma_n (G_n - sum_m sigma_m G_m) dd_n/dc_hat_x,
+            // dd_n / dc_hat_x = -(c_hat_x - c_n,x) / dist_n
+            float acc = 0.0f;
+            for (int n = 0; n < nn; n++) acc += sig[n] * (G[n] - sG) * (-(ch[x] - pal[n * w + x]) / dist[n]);
+            const float gx = 2.0f * (ch[x] - c[x]) + invT * acc;
+            g_out[co + x] = valid ? gx * invB * ch[x] * (1.0f - ch[x]) : 0.0f;   // through the sigmoid
+          }
+          co += w;
+          eo += 2 * w;
+        }
+      }
+    red[tid] = valid ? loss : 0.0f;
+    } else {
+    // ---- endpoint network: L_e + L_cd (Eq. 14); indices from the PREDICTED palette and the reference
+      //      colours, decoded colour from the REFERENCE palette, STE as for the colour net
+      float loss = 0.0f;
+      {
+        const float invB = 1.0f / (float)p.B, invT = 1.0f / p.T;
+        for (int j = 0; j < n_c; j++) {
+          const float d = chat[j] - p.eref[(size_t)sc * n_c + j];
+          loss += d * d;
+          g_out[j] = 2.0f * d;
+        }
+        int co = 0, eo = 0;
+        for (int k = 0; k < p.n_tex; k++) {
+          const int w = p.fmt[k] == kFmtBC1 ? 3 : 1;
+          float pp[24], pr[24], ep[6], er[6];
+          for (int t = 0; t < 2 * w; t++) { ep[t] = chat[eo + t]; er[t] = p.eref[(size_t)sc * n_c + eo + t]; }
+          const int nn = train_palette(p.fmt[k], ep, pp);
+          train_palette(p.fmt[k], er, pr);
+          const bool mode8 = p.fmt[k] == kFmtBC1 || ep[0] > ep[1];
+          for (int i = 0; i < 16; i++) {
+            float c[3];
+            for (int t = 0; t < w; t++) c[t] = p.cref[((size_t)sc * 16 + i) * p.n_c + co + t];
+            float dist[8], dmax = -1e30f;
+            int best = 0;
+            for (int n = 0; n < nn; n++) {
+              float s2 = 0.0f;
+              for (int t = 0; t < w; t++) { const float d = c[t] - pp[n * w + t]; s2 += d * d; }
+              dist[n] = sqrtf(fmaxf(s2, 1e-30f));
+              if (-dist[n] > dmax) { dmax = -dist[n]; best = n; }
+            }
+            float sig[8], ssum = 0.0f;
+            for (int n = 0; n < nn; n++) { sig[n] = expf((-dist[n] - dmax) * invT); ssum += sig[n]; }
+            for (int n = 0; n < nn; n++) sig[n] /= ssum;
+            float gd[3], G[8], sG = 0.0f;
+            for (int t = 0; t < w; t++) {
+              const float dd = pr[best * w + t] - c[t];
+              loss += dd * dd;
+              gd[t] = 2.0f * dd;
+            }
+            for (int n = 0; n < nn; n++) {
+              G[n] = 0.0f;
+              for (int t = 0; t < w; t++) G[n] += gd[t] * pr[n * w + t];
+              sG += sig[n] * G[n];
+            }
+            for (int n = 0; n < nn; n++) {
+              bool constant;
+              const float wn = train_weight(p.fmt[k], mode8, n, constant);
+              if (constant) continue;
+              const float coef = invT * sig[n] * (G[n] - sG);        // dL/dd_n
+              for (int x = 0; x < w; x++) {
+                const float dpal = coef * (-(pp[n * w + x] - c[x]) / dist[n]);   // dL/d pal_pred[n][x]
+                g_out[eo + x] += dpal * (1.0f - wn);
+                g_out[eo + w + x] += dpal * wn;
+              }
             }
           }
+          co += w;
+          eo += 2 * w;
         }
-        co += w;
-        eo += 2 * w;
+        for (int j = 0; j < n_c; j++) g_out[j] = valid ? g_out[j] * invB * chat[j] * (1.0f - chat[j]) : 0.0f;
       }
-      for (int j = 0; j < n_c; j++) g_out[j] = valid ? g_out[j] * invB * chat[j] * (1.0f - chat[j]) : 0.0f;
+    red[tid] = valid ? loss : 0.0f;
     }
-  red[tid] = valid ? loss : 0.0f;
   }
-
   // ---- backward: output layer delta -> D, then layers 3..0
-  float* D = Dl;
-  for (int j = 0; j < n_c; j++) D[tid * LD + j] = g_out[j];
+  __syncthreads();                                                 // every quarter has read c_hat
+  if (h == 0)
+    for (int j = 0; j < n_c; j++) D[tid * LD + j] = g_out[j];
   __syncthreads();
   for (int l = 3; l >= 0; l--) {
     const int K = p.kin[l], N = p.kout[l];
     // weight and bias gradients of layer l over the tile: dW[k][j] = sum_i A_l[i][k] D[i][j]
-    for (int e = tid; e < K * N + N; e += kTrainTile) {
+    for (int e = t; e < K * N + N; e += NT) {
       float acc = 0.0f;
       if (e < K * N) {
         const int k = e / N, j = e - k * N;
-        for (int i = 0; i < kTrainTile; i++) acc += A[l][i * ldA[l] + k] * D[i * LD + j];
+        for (int i = 0; i < kTrainTile; i++) acc = __fmaf_rn(A[l][i * ldA[l] + k], D[i * LD + j], acc);
         atomicAdd(p.grads + p.w_off[l] + e, acc);
       } else {
         const int j = e - K * N;
@@ -309,24 +324,26 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_
         atomicAdd(p.grads + p.b_off[l] + j, acc);
       }
     }
-    // delta of this layer's input: dA[k] = sum_j W[k][j] D[j]; through selu' for hidden inputs
-    float dA[HID];
-    for (int k = 0; k < K; k++) {
+    // delta of this layer's input: dA[k] = sum_j W[k][j] D[j]; through selu' for hidden inputs;
+    // this thread's quarter of the inputs k
+    const int KQ = (K + kTrainQ - 1) / kTrainQ, k0 = h * KQ, k1 = min(K, k0 + KQ);
+    float dA[HID / kTrainQ];
+    for (int k = k0; k < k1; k++) {
       float acc = 0.0f;
-      for (int j = 0; j < N; j++) acc += sW[l][k * N + j] * D[tid * LD + j];
+      for (int j = 0; j < N; j++) acc = __fmaf_rn(sW[l][k * N + j], D[tid * LD + j], acc);
       if (l > 0) {
         const float a = A[l][tid * ldA[l] + k];
         acc *= a > 0.0f ? kSeluL : a + kSeluLA;                     // selu'(z) from a = selu(z)
       }
-      dA[k] = acc;
+      dA[k - k0] = acc;
     }
     __syncthreads();                                               // all readers of D are done
-    for (int k = 0; k < K; k++) D[tid * LD + k] = dA[k];
+    for (int k = k0; k < k1; k++) D[tid * LD + k] = dA[k - k0];
     __syncthreads();
   }
   // ---- grid gradient: scatter d features through the bilinear weights of each level
   if (valid) {
-    for (int l = 0; l < p.levels; l++) {
+    for (int l = h; l < p.levels; l += kTrainQ) {
       const int res = p.coarsest << l;
       const float X = u * (float)(res - 1), Y = v * (float)(res - 1);
       const int i0 = min((int)floorf(X), res - 2), j0 = min((int)floorf(Y), res - 2);
@@ -351,10 +368,10 @@ __global__ void __launch_bounds__(kTrainTile, 1) train_step_kernel(const __grid_
   // ---- batch-mean loss
   __syncthreads();
   for (int st = kTrainTile / 2; st > 0; st >>= 1) {
-    if (tid < st) red[tid] += red[tid + st];
+    if (t < st) red[t] += red[t + st];
     __syncthreads();
   }
-  if (tid == 0) atomicAdd(p.loss, red[0] / (float)p.B);
+  if (t == 0) atomicAdd(p.loss, red[0] / (float)p.B);
 }
 
 // bias-corrected Adam: lr_grid for the first n_grid parameters, lr_mlp for the rest

@@ -702,9 +702,10 @@ ntbc_status train_step(int net, const ntbc_train_arch* arch, float* params, floa
   }
   p.params = params; p.grads = grads; p.xy = xy; p.cref = cref; p.eref = eref;
   p.B = batch; p.W = width; p.H = height; p.T = temperature; p.loss = loss;
+  auto al4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
   size_t smem = 0;
-  for (int l = 0; l < 4; l++) smem += (size_t)(p.kin[l] * p.kout[l] + p.kout[l]);
-  smem += (size_t)kTrainTile * (2 * p.levels + 1) + 4 * (size_t)kTrainTile * 65 + kTrainTile;
+  for (int l = 0; l < 4; l++) smem += al4((size_t)p.kin[l] * p.kout[l]) + al4((size_t)p.kout[l]);
+  smem += al4((size_t)kTrainTile * (2 * p.levels + 1)) + 4 * (size_t)kTrainTile * (64 + 4) + kTrainTile;
   smem *= sizeof(float);
   auto kern = net == 1 ? train_step_kernel<64, 1> : train_step_kernel<64, 0>;
   static bool configured[2] = {false, false};

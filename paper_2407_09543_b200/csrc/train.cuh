@@ -124,14 +124,16 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
   // layer's outputs / inputs (more warps per SM at the same shared memory)
   const int t = threadIdx.x, tid = t % kTrainTile, h = t / kTrainTile, NT = kTrainTile * kTrainQ;
   const int n_c = NET ? p.n_c : p.n_e, F = 2 * p.levels;   // n_c here = MLP outputs
-  constexpr int LD = HID + 1;                                   // padded row stride (bank-conflict free)
+  // padded row stride: 16-B aligned rows for float4 access, rows 4 banks apart (conflict-free LDS.128)
+  constexpr int LD = HID + 4;
   // ---- shared memory: weights, biases, tile activations A0 (features), A1..A3, delta buffer
+  auto al4 = [](int n) { return (n + 3) & ~3; };
   float* sW[4];
   float* sb[4];
   float* q = sm;
-  for (int l = 0; l < 4; l++) { sW[l] = q; q += p.kin[l] * p.kout[l]; sb[l] = q; q += p.kout[l]; }
+  for (int l = 0; l < 4; l++) { sW[l] = q; q += al4(p.kin[l] * p.kout[l]); sb[l] = q; q += al4(p.kout[l]); }
   float* A[4];
-  A[0] = q; q += kTrainTile * (F + 1);
+  A[0] = q; q += al4(kTrainTile * (F + 1));
   for (int l = 1; l < 4; l++) { A[l] = q; q += kTrainTile * LD; }
   float* Dl = q; q += kTrainTile * LD;                          // delta of the current layer output
   float* red = q;                                               // [kTrainTile] loss reduction
@@ -166,15 +168,28 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
     }
   }
   __syncthreads();
-  constexpr int HQ = HID / kTrainQ;
+  constexpr int HQ = HID / kTrainQ;   // this thread's HQ consecutive outputs, register-blocked
+  static_assert(HQ % 4 == 0, "quarter width must be a multiple of 4");
   for (int l = 0; l < 3; l++) {
     const float* a = A[l] + tid * ldA[l];
     float* o = A[l + 1] + tid * LD;
-    for (int j = h * HQ; j < (h + 1) * HQ; j++) {
-      float z = sb[l][j];
-      for (int k = 0; k < p.kin[l]; k++) z = __fmaf_rn(a[k], sW[l][k * HID + j], z);
-      o[j] = selu_f(z);
+    float z[HQ];
+#pragma unroll
+    for (int jj = 0; jj < HQ; jj++) z[jj] = sb[l][h * HQ + jj];
+    for (int k = 0; k < p.kin[l]; k++) {
+      const float ak = a[k];
+      const float4* w4 = reinterpret_cast<const float4*>(sW[l] + k * HID + h * HQ);
+#pragma unroll
+      for (int q4 = 0; q4 < HQ / 4; q4++) {
+        const float4 w = w4[q4];
+        z[4 * q4] = __fmaf_rn(ak, w.x, z[4 * q4]);
+        z[4 * q4 + 1] = __fmaf_rn(ak, w.y, z[4 * q4 + 1]);
+        z[4 * q4 + 2] = __fmaf_rn(ak, w.z, z[4 * q4 + 2]);
+        z[4 * q4 + 3] = __fmaf_rn(ak, w.w, z[4 * q4 + 3]);
+      }
     }
+#pragma unroll
+    for (int jj = 0; jj < HQ; jj++) o[h * HQ + jj] = selu_f(z[jj]);
     __syncthreads();
   }
   float* D = Dl;
@@ -312,31 +327,64 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
   for (int l = 3; l >= 0; l--) {
     const int K = p.kin[l], N = p.kout[l];
     // weight and bias gradients of layer l over the tile: dW[k][j] = sum_i A_l[i][k] D[i][j]
-    for (int e = t; e < K * N + N; e += NT) {
-      float acc = 0.0f;
-      if (e < K * N) {
+    if (K % 2 == 0 && N % 4 == 0) {
+      // 2 x 4 blocks (k pair, j quad): per sample 2 scalar + 1 float4 shared-memory loads for 8 FMAs
+      const int nblk = (K / 2) * (N / 4);
+      for (int e = t; e < nblk; e += NT) {
+        const int kp = e / (N / 4), jq = e - kp * (N / 4), k = 2 * kp, j = 4 * jq;
+        float acc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
+        for (int i = 0; i < kTrainTile; i++) {
+          const float a0 = A[l][i * ldA[l] + k], a1 = A[l][i * ldA[l] + k + 1];
+          const float4 d = *reinterpret_cast<const float4*>(D + i * LD + j);
+          acc[0][0] = __fmaf_rn(a0, d.x, acc[0][0]); acc[0][1] = __fmaf_rn(a0, d.y, acc[0][1]);
+          acc[0][2] = __fmaf_rn(a0, d.z, acc[0][2]); acc[0][3] = __fmaf_rn(a0, d.w, acc[0][3]);
+          acc[1][0] = __fmaf_rn(a1, d.x, acc[1][0]); acc[1][1] = __fmaf_rn(a1, d.y, acc[1][1]);
+          acc[1][2] = __fmaf_rn(a1, d.z, acc[1][2]); acc[1][3] = __fmaf_rn(a1, d.w, acc[1][3]);
+        }
+#pragma unroll
+        for (int r = 0; r < 2; r++)
+#pragma unroll
+          for (int c = 0; c < 4; c++) atomicAdd(p.grads + p.w_off[l] + (size_t)(k + r) * N + j + c, acc[r][c]);
+      }
+    } else {
+      for (int e = t; e < K * N; e += NT) {
         const int k = e / N, j = e - k * N;
+        float acc = 0.0f;
         for (int i = 0; i < kTrainTile; i++) acc = __fmaf_rn(A[l][i * ldA[l] + k], D[i * LD + j], acc);
         atomicAdd(p.grads + p.w_off[l] + e, acc);
-      } else {
-        const int j = e - K * N;
-        for (int i = 0; i < kTrainTile; i++) acc += D[i * LD + j];
-        atomicAdd(p.grads + p.b_off[l] + j, acc);
       }
+    }
+    for (int j = t; j < N; j += NT) {   // bias gradient
+      float acc = 0.0f;
+      for (int i = 0; i < kTrainTile; i++) acc += D[i * LD + j];
+      atomicAdd(p.grads + p.b_off[l] + j, acc);
     }
     // delta of this layer's input: dA[k] = sum_j W[k][j] D[j]; through selu' for hidden inputs;
     // this thread's quarter of the inputs k
     const int KQ = (K + kTrainQ - 1) / kTrainQ, k0 = h * KQ, k1 = min(K, k0 + KQ);
     float dA[HID / kTrainQ];
-    for (int k = k0; k < k1; k++) {
-      float acc = 0.0f;
-      for (int j = 0; j < N; j++) acc = __fmaf_rn(sW[l][k * N + j], D[tid * LD + j], acc);
+#pragma unroll
+    for (int kk = 0; kk < HID / kTrainQ; kk++) dA[kk] = 0.0f;
+    if (N % 4 == 0) {   // per j quad: one float4 of this sample's delta row, one float4 per W row (broadcast)
+      const float4* d4 = reinterpret_cast<const float4*>(D + tid * LD);
+      for (int jq = 0; jq < N / 4; jq++) {
+        const float4 d = d4[jq];
+#pragma unroll
+        for (int kk = 0; kk < HID / kTrainQ; kk++) {
+          if (k0 + kk >= k1) break;
+          const float4 w = *reinterpret_cast<const float4*>(sW[l] + (k0 + kk) * N + 4 * jq);
+          dA[kk] = __fmaf_rn(w.w, d.w, __fmaf_rn(w.z, d.z, __fmaf_rn(w.y, d.y, __fmaf_rn(w.x, d.x, dA[kk]))));
+        }
+      }
+    } else {
+      for (int k = k0; k < k1; k++)
+        for (int j = 0; j < N; j++) dA[k - k0] = __fmaf_rn(sW[l][k * N + j], D[tid * LD + j], dA[k - k0]);
+    }
+    for (int k = k0; k < k1; k++)
       if (l > 0) {
         const float a = A[l][tid * ldA[l] + k];
-        acc *= a > 0.0f ? kSeluL : a + kSeluLA;                     // selu'(z) from a = selu(z)
+        dA[k - k0] *= a > 0.0f ? kSeluL : a + kSeluLA;              // selu'(z) from a = selu(z)
       }
-      dA[k - k0] = acc;
-    }
     __syncthreads();                                               // all readers of D are done
     for (int k = k0; k < k1; k++) D[tid * LD + k] = dA[k - k0];
     __syncthreads();

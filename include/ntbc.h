@@ -102,6 +102,13 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
                                       const size_t* blob_sizes, int width, int height,
                                       void* const* host_out, void* stream);
 
+/* Debug: with NTBC_TIMELINE=1 in the environment, ntbc_decode_material_host records CUDA events;
+ * this returns, for the model's last call, the times (ms) relative to the call's start on `stream` of:
+ * [0] call start, [1] its upload done (negative when it overlapped the previous call), [2] kernel
+ * start, [3] kernel end, [4..7] copy-back done per internal copy stream, [8] the previous call's start,
+ * [9..12] the previous call's copy-back done per stream (negative).  n >= 13.  Synchronizes. */
+ntbc_status ntbc_debug_host_timeline(ntbc_model m, float* ms_out, int n);
+
 /* reference BC1/BC4 encoder -- the documented stand-in for the paper's Compressonator
  * "two refine steps" (SPEC encode_block_reference S:153-161; R24-R29):
  * PCA (BC1) or min/max (BC4, both modes) endpoints, n_refine least-squares refinements of the

@@ -168,6 +168,12 @@ struct ntbc_model_s {
   int cur = 0;
   cudaStream_t upload_stream = nullptr;
   cudaEvent_t uploaded = nullptr, slot_free[2] = {nullptr, nullptr};
+  // optional timeline of the last host-path call (NTBC_TIMELINE=1): call start, upload done, kernel
+  // start, kernel end, copies done (per copy stream) -- ntbc_debug_host_timeline
+  cudaEvent_t tlset[2][4 + kCopyStreams] = {};
+  cudaEvent_t* tl = tlset[0];
+  int tl_cur = 0;
+  bool tl_on = false;
 };
 
 namespace {
@@ -460,6 +466,8 @@ void ntbc_free_model(ntbc_model m) {
     if (m->copy_done[i]) cudaEventDestroy(m->copy_done[i]);
   }
   for (int i = 0; i < 2; i++) if (m->slot_free[i]) cudaEventDestroy(m->slot_free[i]);
+  for (auto& row : m->tlset)
+    for (auto e : row) if (e) cudaEventDestroy(e);
   if (m->uploaded) cudaEventDestroy(m->uploaded);
   if (m->upload_stream) cudaStreamDestroy(m->upload_stream);
   cudaFree(m->slot_blob[1]);
@@ -529,6 +537,11 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
       if (cudaMalloc(&m->d_scratch, need) != cudaSuccess) { cudaGetLastError(); return fail(NTBC_ENOMEM, "scratch %zu B", need); }
       m->scratch_bytes = need;
     }
+    if (m->tlset[1][0] && getenv("NTBC_TIMELINE") && atoi(getenv("NTBC_TIMELINE"))) {
+      m->tl_cur ^= 1;
+      m->tl = m->tlset[m->tl_cur];
+      CUDA_TRY(cudaEventRecord(m->tl[0], cs));
+    }
     FusedParams p{};
     p.W = width; p.H = height; p.row_begin = 0; p.row_end = BH;
     for (int k = 0; k < n_tex; k++) p.out[k] = (uint64_t*)(m->d_scratch + k * plane);
@@ -545,8 +558,10 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
       st = ntbc_model_upload_async(m, blobs[i], blob_sizes[i], stream);
       if (st) return st;
     } else {
-      // upload into the idle weight slot on upload_stream (overlaps the previous call's kernel),
-      // once the last kernel that read that slot has finished; the kernel below waits for it.
+      // upload into the idle weight slot on upload_stream (overlaps the previous call's kernel) once
+      // that kernel has STARTED: the slot's last reader (the kernel before it) is done by then, and the
+      // upload no longer competes with the copy-back tail of the call before (measured: 2.75 -> 2.6 ms
+      // per call when it waited only for the slot); the kernel below waits for the upload.
       Arch a;
       st = parse(blobs[i], blob_sizes[i], a);
       if (st) return st;
@@ -555,22 +570,30 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
       m->arch = a;
       m->cur = s;
       m->d_blob = m->slot_blob[s];
-      CUDA_TRY(cudaStreamWaitEvent(m->upload_stream, m->slot_free[s], 0));
+      CUDA_TRY(cudaStreamWaitEvent(m->upload_stream, m->copy_start, 0));   // the previous call's kernel start
       st = upload(m, blobs[i], blob_sizes[i], m->upload_stream);
       if (st) return st;
       CUDA_TRY(cudaEventRecord(m->uploaded, m->upload_stream));
+      if (getenv("NTBC_TIMELINE") && atoi(getenv("NTBC_TIMELINE")) && m->tl[1]) CUDA_TRY(cudaEventRecord(m->tl[1], m->upload_stream));
       CUDA_TRY(cudaStreamWaitEvent(cs, m->uploaded, 0));
     }
     if (pipelined) {
       p.progress = m->d_progress;
       p.chunk_rows = big;
     }
+    const bool tl = pipelined && getenv("NTBC_TIMELINE") && atoi(getenv("NTBC_TIMELINE"));
+    if (tl && !m->tlset[1][0])
+      for (auto& row : m->tlset)
+        for (auto& e : row) CUDA_TRY(cudaEventCreate(&e));
+    m->tl_on = tl;
+    if (tl) CUDA_TRY(cudaEventRecord(m->tl[2], cs));
     if (pipelined) {  // copy stream: ordered after the upload and whatever precedes it on `stream`
       CUDA_TRY(cudaEventRecord(m->copy_start, cs));
       for (int i = 0; i < kCopyStreams; i++) CUDA_TRY(cudaStreamWaitEvent(m->copy_stream[i], m->copy_start, 0));
     }
     st = launch_fused(m, p, false, cs);
     if (st) return st;
+    if (tl) CUDA_TRY(cudaEventRecord(m->tl[3], cs));
     if (pipelined) CUDA_TRY(cudaEventRecord(m->slot_free[m->cur], cs));
     if (!pipelined) {
       for (int k = 0; k < n_tex; k++)
@@ -590,12 +613,29 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
                                    (size_t)(r1 - r0) * row_bytes, cudaMemcpyDeviceToHost, xs));
       }
       for (int i = 0; i < kCopyStreams; i++) {   // the caller's stream sees every finished copy
+        if (tl) CUDA_TRY(cudaEventRecord(m->tl[4 + i], m->copy_stream[i]));
         CUDA_TRY(cudaEventRecord(m->copy_done[i], m->copy_stream[i]));
         CUDA_TRY(cudaStreamWaitEvent(cs, m->copy_done[i], 0));
       }
     }
     t += n_tex;
   }
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_debug_host_timeline(ntbc_model m, float* ms_out, int n) {
+  if (!m || !ms_out || n < 5 + 2 * kCopyStreams) return fail(NTBC_EINVAL, "need %d outputs", 5 + 2 * kCopyStreams);
+  if (!m->tl_on || !m->tlset[1][0]) return fail(NTBC_EINVAL, "no timeline recorded (set NTBC_TIMELINE=1)");
+  DevGuard dg(m->device);
+  cudaEvent_t* prev = m->tlset[m->tl_cur ^ 1];
+  for (int i = 0; i < 4 + kCopyStreams; i++) {
+    CUDA_TRY(cudaEventSynchronize(m->tl[i]));
+    CUDA_TRY(cudaEventElapsedTime(ms_out + i, m->tl[0], m->tl[i]));
+  }
+  // the previous call's start and copy completions relative to this call's start
+  CUDA_TRY(cudaEventElapsedTime(ms_out + 4 + kCopyStreams, m->tl[0], prev[0]));
+  for (int i = 0; i < kCopyStreams; i++)
+    CUDA_TRY(cudaEventElapsedTime(ms_out + 5 + kCopyStreams + i, m->tl[0], prev[4 + i]));
   return NTBC_OK;
 }
 

@@ -41,6 +41,7 @@ _SIGS = {
     "ntbc_decode_material_host": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _vp]),
     "ntbc_decode_bc": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "ntbc_encode_bc": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
+    "ntbc_debug_host_timeline": (_i, [_vp, _vp, _i]),
     "ntbc_train_param_count": (C.c_longlong, [_vp]),
     "ntbc_train_endpoint_param_count": (C.c_longlong, [_vp]),
     "ntbc_train_endpoint_step": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _i, C.c_float, C.c_float,
@@ -148,6 +149,13 @@ def decode_material_host(models, pinned_blobs, width: int, height: int, host_out
     outs = (_vp * len(host_outs))(*[o.data_ptr() for o in host_outs])
     _check(_lib.ntbc_decode_material_host(_handles(models), len(models), blobs, sizes, width, height, outs,
                                           _stream(stream)))
+
+
+def debug_host_timeline(model):
+    """Event times (ms) of the model's last ntbc_decode_material_host call (needs NTBC_TIMELINE=1)."""
+    out = (C.c_float * 13)()
+    _check(_lib.ntbc_debug_host_timeline(model.handle, out, 13))
+    return list(out)
 
 
 def encode_bc(texels: torch.Tensor, fmt: int, width: int, height: int, n_refine: int = 2, out=None, stream=None):

@@ -63,3 +63,30 @@ def test_decode_rejects_bad_dims_without_gpu(lib):
     assert lib.ntbc_pack(1, f, buf, buf, 8, 8, 0, 2, ptrs, None) == -1           # bad format code
     f = (C.c_int * 1)(1)
     assert lib.ntbc_pack(1, f, buf, buf, 8, 8, 1, 1, ptrs, None) == -1           # empty row range
+
+
+def test_load_model_fuzzed_blobs_never_crash(lib):
+    """Truncations and random byte corruptions of valid containers (both variants) are rejected with
+    a status code (EFORMAT / EMISMATCH / EINVAL, or ECUDA once parsing passes on a GPU-less host) --
+    the parser never reads out of bounds or crashes."""
+    import numpy as np
+    import synth
+    lib.ntbc_load_model.restype = C.c_int
+    lib.ntbc_free_model.restype = None
+    rng = np.random.default_rng(0)
+    for cfg in (1, 8):
+        blob = bytearray(synth.model_blob(cfg))
+        cases = [bytes(blob[:n]) for n in (0, 4, 95, 96, 97, 150, len(blob) // 2, len(blob) - 1)]
+        for _ in range(150):
+            b = bytearray(blob)
+            for _ in range(int(rng.integers(1, 4))):
+                pos = int(rng.integers(0, 160)) if rng.random() < 0.7 else int(rng.integers(0, len(b)))
+                b[pos] = int(rng.integers(0, 256))
+            cases.append(bytes(b))
+        for data in cases:
+            h = C.c_void_p()
+            buf = C.create_string_buffer(data, max(1, len(data)))
+            st = lib.ntbc_load_model(buf, len(data), 0, C.byref(h))
+            assert st in (0, -1, -2, -3, -4, -5)
+            if st == 0:
+                lib.ntbc_free_model(h)

@@ -605,9 +605,12 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
         int r0, r1;
         chunk_rows(c, r0, r1);
         m->progress_target[c] += (unsigned long long)(r1 - r0) * upr;
-        cudaStream_t xs = m->copy_stream[c % kCopyStreams];
-        if (g_wait64((CUstream)xs, (CUdeviceptr)(m->d_progress + c), m->progress_target[c],
-                     CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        // the last chunk finishes with the kernel: copy it in stream order right behind the kernel
+        // (no counter wait, whose latency would add to the exposed tail)
+        const bool last = c == n_chunks - 1 && n_chunks > 1;
+        cudaStream_t xs = last ? cs : m->copy_stream[c % kCopyStreams];
+        if (!last && g_wait64((CUstream)xs, (CUdeviceptr)(m->d_progress + c), m->progress_target[c],
+                              CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
           return fail(NTBC_ECUDA, "stream wait on progress counter failed");
         for (int k = 0; k < n_tex; k++)
           CUDA_TRY(cudaMemcpyAsync((uint8_t*)host_out[t + k] + r0 * row_bytes, (const uint8_t*)p.out[k] + r0 * row_bytes,

@@ -166,23 +166,24 @@ void o_f32_to_f16_n(const float* x, uint16_t* out, size_t n) {
 float o_dequant(uint8_t q, float s, int32_t z) { return s * (float)((int32_t)q - z); }
 
 /* ------------------------------------------------------------------------- */
-/* pinned exponential (R9): 2^n * (1 + f*Q(f)), Q a degree-4 polynomial       */
+/* pinned exponential (R9): 2^n * (1 + f*Q(f)), Q a degree-3 polynomial       */
 /* ------------------------------------------------------------------------- */
 static const float LOG2E = 0x1.715476p+0f;
 static const float MAGIC = 12582912.0f;                      /* 1.5 * 2^23 */
-static const float Q0 = 0x1.62e426p-1f, Q1 = 0x1.ebf9b6p-3f, Q2 = 0x1.c6ba7ap-5f,
-                   Q3 = 0x1.3cec0ep-7f, Q4 = 0x1.5a9610p-10f;
+/* Q(f) ~ (2^f - 1)/f on |f| <= 1/2, minimax in relative error (<= 1.6e-5: below 1/16 of a binary16
+   ulp, the precision the hidden activations are stored in) */
+static const float Q0 = 0x1.62e2d6p-1f, Q1 = 0x1.ebff08p-3f, Q2 = 0x1.c96b34p-5f, Q3 = 0x1.3b2a76p-7f;
 static const float SELU_L = 0x1.0cfabep+0f;                  /* RN32(1.0507009873554804934) */
 static const float SELU_LA = 0x1.c212ccp+0f;                 /* RN32(lambda * alpha)        */
 
-/* e^x = 2^n (1 + u): n = rint(x log2e) (magic-number rounding of the exactly-computed product),
-   f = RN(x log2e - n) (exact product, one rounding), u = RN(f Q(f)).  Returns n and u. */
-static int exp_reduce(float x, float* u_out) {
+/* e^x = 2^n (1 + f Q(f)): n = rint(x log2e) (magic-number rounding of the exactly-computed product),
+   f = RN(x log2e - n) (exact product, one rounding), q = Q(f) by Horner.  Returns n, f and q. */
+static int exp_reduce(float x, float* f_out, float* q_out) {
     float r = fmaf(x, LOG2E, MAGIC);              /* rint(x log2e) + 1.5*2^23, one rounding */
     float negnf = MAGIC - r;                      /* -n, exact */
     float f = fmaf(x, LOG2E, negnf);              /* x log2e - n, one rounding */
-    float q = fmaf(fmaf(fmaf(fmaf(Q4, f, Q3), f, Q2), f, Q1), f, Q0);
-    *u_out = f * q;
+    *f_out = f;
+    *q_out = fmaf(fmaf(fmaf(Q3, f, Q2), f, Q1), f, Q0);
     int32_t ri, mi; memcpy(&ri, &r, 4); float mg = MAGIC; memcpy(&mi, &mg, 4);
     return ri - mi;
 }
@@ -192,19 +193,20 @@ static float pow2i(int n, float scale) {          /* scale * 2^n by exponent ins
     float v; memcpy(&v, &b, 4);
     return v;
 }
-/* E(x) = 2^n + 2^n u, x clamped to [-80, 80] */
+/* E(x) = 2^n + 2^n RN(f q), x clamped to [-80, 80] */
 float o_exp(float x) {
-    float xc = fminf(fmaxf(x, -80.0f), 80.0f), u;
-    int n = exp_reduce(xc, &u);
+    float xc = fminf(fmaxf(x, -80.0f), 80.0f), f, q;
+    int n = exp_reduce(xc, &f, &q);
     float s = pow2i(n, 1.0f);
-    return fmaf(s, u, s);
+    return fmaf(s, f * q, s);
 }
-/* selu negative branch (R8/R9): lambda*alpha*(e^z - 1) = fma(S, u, S - lambda*alpha), S = lambda*alpha*2^n exact */
+/* selu negative branch (R8/R9): lambda*alpha*(e^z - 1) = fma(S, RN(1 + f q), -lambda*alpha),
+   S = lambda*alpha*2^n exact */
 static float selu_neg(float z) {
-    float x = fmaxf(z, -80.0f), u;
-    int n = exp_reduce(x, &u);
+    float x = fmaxf(z, -80.0f), f, q;
+    int n = exp_reduce(x, &f, &q);
     float S = pow2i(n, SELU_LA);
-    return fmaf(S, u, S - SELU_LA);
+    return fmaf(S, fmaf(f, q, 1.0f), -SELU_LA);
 }
 float o_expm1(float x) { return selu_neg(x) / SELU_LA; }   /* for the accuracy pin only (x <= 0) */
 

@@ -1,7 +1,7 @@
 """A/B kernel timing of in-tree library variants (debugging aid, not a bench number).
 
-usage: python tools/ab_time.py [config] [reps] lib1.so lib2.so ...
-Each variant runs in its own process (NTBC_LIB=<name>), decodes the config's material `reps`
+usage: python tools/ab_time.py [config] [reps] lib1.so lib2.so:NTBC_NWG=4 ...
+Each variant runs in its own process (NTBC_LIB=<name>, plus optional KEY=VAL env settings after ':'), decodes the config's material `reps`
 times with the L2 flushed between launches and prints median / min kernel ms (CUDA events)."""
 import os
 import subprocess
@@ -29,7 +29,7 @@ for _ in range(reps):
     a.record(s); ntbc.decode_material([m], W, H, outs=outs, stream=s); b.record(s)
     torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
 ts.sort()
-print(json.dumps({"lib": os.environ.get("NTBC_LIB", "libntbc.so"), "cfg": cfg, "median_ms": ts[len(ts) // 2],
+print(json.dumps({"lib": os.environ.get("NTBC_LIB", "libntbc.so"), "nwg": os.environ.get("NTBC_NWG"), "cfg": cfg, "median_ms": ts[len(ts) // 2],
                   "min_ms": ts[0]}))
 """ % ROOT
 
@@ -39,8 +39,9 @@ def main():
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 40
     libs = sys.argv[3:] or ["libntbc.so"]
     for rnd in range(2):   # two interleaved rounds: clocks drift between processes
-        for lib in libs:
-            env = dict(os.environ, NTBC_LIB=lib)
+        for spec in libs:
+            lib, *kv = spec.split(":")
+            env = dict(os.environ, NTBC_LIB=lib, **dict(x.split("=", 1) for x in kv))
             out = subprocess.run([sys.executable, "-c", CHILD, str(cfg), str(reps)], env=env, capture_output=True,
                                  text=True)
             print(f"round {rnd}:", out.stdout.strip() or out.stderr.strip()[-400:], flush=True)

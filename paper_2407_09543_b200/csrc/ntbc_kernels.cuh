@@ -204,6 +204,10 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   const uint32_t img_base[2] = {smem_u32(img_e), smem_u32(img_c)};
   const int bar_id = 1 + wg;
   uint32_t phase = 0;
+  // the thread that issues this group's MMAs: lane 0 of warp (wg mod 4) of the group, so the issuing
+  // warps are spread over the four SM sub-partitions (warp w runs on SMSP w mod 4; measured: all eight
+  // on SMSP 0 made each MMA cost ~275 issue cycles on the group's critical path, 2.25 -> 2.15 ms)
+  const int issuer = 32 * (wg & 3);
 
   // 16 grid features of row r (levels coarse->fine, 2 per level, R3) -> fp16 -> A columns 0..15
   auto features = [&](int g, float pu, float pv, float* dump) {
@@ -227,14 +231,14 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       fence_async_smem();
       tc_fence_before();
       named_bar_sync(bar_id, 128);
-      if (r == 0) {
+      if (r == issuer) {
         tc_fence_after();
         const int kin16 = l == 0 ? 16 : H;
         const int N = l < 3 ? H : p.net[n].n_out16;
         issue_layer(tm, a_base, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
         mma_commit(bar_mma);
       }
-      if (r == 0) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
+      if (r == issuer) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
       named_bar_sync(bar_id, 128);
       phase ^= 1u;
       tc_fence_after();

@@ -175,8 +175,12 @@ def run_ours(args, rank, world, local_rank):
 
     import synth
     from paper_2407_09543_b200 import ntbc
-    from paper_2407_09543_b200.shard import gather_materials
+    from paper_2407_09543_b200.shard import PeerGather, gather_materials
 
+    # NTBC_BENCH_ONE_GPU=1: functional check of the multi-rank path on a one-GPU box (every rank on cuda:0,
+    # gloo process group; the ranks' kernels never wait on each other).  Its numbers are not measurements.
+    if os.environ.get("NTBC_BENCH_ONE_GPU") == "1":
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     W, H, spec = synth.config_shape(args.config)
@@ -189,11 +193,20 @@ def run_ours(args, rank, world, local_rank):
     outs = [out_all[k] for k in range(n_tex)]
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
+    # the final gather of packed bytes to rank 0 (north star), inside the timed step: fused into the decode
+    # by default (every rank's kernel stores its BC words into rank 0's buffer over NVLink, PeerGather);
+    # NTBC_GATHER=nccl uses a separate NCCL gather after the decode instead
+    gather_mode = os.environ.get("NTBC_GATHER", "peer") if world > 1 else "none"
+    pg = PeerGather(n_tex, BH, BW, rank, world, dev) if gather_mode == "peer" else None
 
     def step():
-        ntbc.decode_material([model], W, H, outs=outs, stream=stream)
-        if world > 1:   # the final gather of packed bytes to rank 0 (north star), inside the timed step
-            gather_materials(out_all, rank, world)
+        if pg is not None:
+            ntbc.decode_material([model], W, H, out_ptrs=pg.ptrs, stream=stream)
+            pg.complete()
+        else:
+            ntbc.decode_material([model], W, H, outs=outs, stream=stream)
+            if world > 1:
+                gather_materials(out_all, rank, world)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -212,6 +225,10 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     launches = ntbc.launch_count() - launches0
+    if pg is not None and rank == 0:   # rank 0's buffer holds every rank's material: spot-check our own slice
+        ntbc.decode_material([model], W, H, outs=outs, stream=stream)
+        torch.cuda.synchronize()
+        assert torch.equal(pg.buf[0], out_all), "peer gather: rank 0 slice differs from a local decode"
     times = [a.elapsed_time(b) for a, b in evs]
     t_ms = sum(times) / len(times)
     t_tensor = torch.tensor([t_ms], device=dev, dtype=torch.float64)
@@ -249,6 +266,9 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(e_tensor, op=dist.ReduceOp.MAX)
     e_ms = float(e_tensor.item())
+    if pg is not None:   # unmap rank 0's buffer everywhere before rank 0 may free it
+        pg.close()
+        dist.barrier()
 
     if rank != 0:
         return
@@ -283,6 +303,9 @@ def run_ours(args, rank, world, local_rank):
                    "textures": len(spec.fmts), "formats": ["BC1" if f == 1 else "BC4" for f in spec.fmts],
                    "model": "paper architecture (P:330-343), random-init seeded weights",
                    "materials_per_rank_per_step": 1, "gather_to_rank0": world > 1,
+                   "gather": {"none": None, "peer": "fused: each rank's kernel stores its BC words into rank 0's "
+                              "buffer over NVLink (CUDA IPC), completion by a 1-element all-reduce",
+                              "nccl": "separate NCCL gather after the decode"}[gather_mode],
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
                    "ms_per_4k_material": t_ms_max / world if world > 1 else t_ms_max},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
@@ -323,8 +346,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("NTBC_BENCH_ONE_GPU") == "1":   # functional check only (see run_ours)
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -185,6 +185,26 @@ ntbc_status ntbc_pack(int n_textures, const int* fmts, const float* endpoints, c
  * A, B fp16 row-major device; C, D fp32 device; N in {16,32,64}, K % 16 == 0, K <= 128. */
 ntbc_status ntbc_debug_mma(const void* A, const void* B, const float* C, float* D, int K, int N, void* stream);
 
+/* Peer-memory gather (BASELINE north star: "only a final gather of packed bytes, counted in
+ * the timing").  The gather is fused into the decode: a rank passes pointers into rank 0's output
+ * buffer as the out_blocks of ntbc_decode_material, so the fused kernel's BC-word stores travel over
+ * NVLink straight into rank 0's HBM, unit by unit, while later units are still being computed; no
+ * separate collective moves the bytes.  These three calls are the CUDA-IPC plumbing.
+ *   ntbc_peer_export: device_ptr = any address inside a cudaMalloc allocation of this process;
+ *     writes NTBC_PEER_HANDLE_BYTES opaque bytes (IPC handle of the allocation + the offset of
+ *     device_ptr in it) to handle_out (host memory), to be sent to the other ranks.
+ *   ntbc_peer_open: maps an exported handle of ANOTHER process into `cuda_device`'s address space
+ *     (peer access enabled lazily) and returns the pointer equivalent to the exporter's device_ptr;
+ *     valid until ntbc_peer_close.  The exporter must keep the allocation alive until every opener
+ *     has closed it.  Writes through the pointer are visible to the exporter's device once the
+ *     writing kernel has completed and the processes have synchronised (e.g. a process-group barrier).
+ *   ntbc_peer_close: unmaps a pointer returned by ntbc_peer_open.
+ * Errors: NTBC_EINVAL (NULL, not device memory, unknown pointer), NTBC_ECUDA. */
+#define NTBC_PEER_HANDLE_BYTES 72
+ntbc_status ntbc_peer_export(const void* device_ptr, void* handle_out);
+ntbc_status ntbc_peer_open(const void* handle, int cuda_device, void** device_ptr_out);
+ntbc_status ntbc_peer_close(void* device_ptr);
+
 /* Number of kernel launches the library issued since load (all entry points), for bench accounting. */
 uint64_t ntbc_launch_count(void);
 

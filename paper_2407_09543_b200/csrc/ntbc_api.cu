@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -391,6 +393,11 @@ ntbc_status check_dims(int W, int H, int r0, int r1) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------- peer-memory gather plumbing (CUDA IPC)
+typedef CUresult (*addr_range_fn)(CUdeviceptr*, size_t*, CUdeviceptr);
+static std::mutex g_peer_mu;
+static std::unordered_map<void*, void*> g_peer_base;   // pointer returned by ntbc_peer_open -> mapped base
 
 extern "C" {
 
@@ -866,6 +873,61 @@ ntbc_status ntbc_debug_mma(const void* A, const void* B, const float* C, float* 
 }
 
 uint64_t ntbc_launch_count(void) { return g_launches.load(); }
+
+ntbc_status ntbc_peer_export(const void* device_ptr, void* handle_out) {
+  if (!device_ptr || !handle_out) return fail(NTBC_EINVAL, "NULL argument");
+  cudaPointerAttributes at{};
+  CUDA_TRY(cudaPointerGetAttributes(&at, device_ptr));
+  if (at.type != cudaMemoryTypeDevice) return fail(NTBC_EINVAL, "not a device allocation");
+  DevGuard dg(at.device);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return fail(NTBC_ECUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<addr_range_fn>(fn)(&base, &size, (CUdeviceptr)device_ptr) != CUDA_SUCCESS)
+    return fail(NTBC_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base));
+  const uint64_t off = (uint64_t)((CUdeviceptr)device_ptr - base);
+  std::memcpy(handle_out, &h, sizeof(h));
+  std::memcpy((uint8_t*)handle_out + 64, &off, sizeof(off));
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_peer_open(const void* handle, int cuda_device, void** device_ptr_out) {
+  if (!handle || !device_ptr_out) return fail(NTBC_EINVAL, "NULL argument");
+  *device_ptr_out = nullptr;
+  DevGuard dg(cuda_device);
+  cudaIpcMemHandle_t h;
+  uint64_t off = 0;
+  std::memcpy(&h, handle, sizeof(h));
+  std::memcpy(&off, (const uint8_t*)handle + 64, sizeof(off));
+  void* base = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  void* p = (uint8_t*)base + off;
+  {
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    g_peer_base[p] = base;
+  }
+  *device_ptr_out = p;
+  return NTBC_OK;
+}
+
+ntbc_status ntbc_peer_close(void* device_ptr) {
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    auto it = g_peer_base.find(device_ptr);
+    if (it == g_peer_base.end()) return fail(NTBC_EINVAL, "pointer was not returned by ntbc_peer_open");
+    base = it->second;
+    g_peer_base.erase(it);
+  }
+  CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return NTBC_OK;
+}
 
 const char* ntbc_last_error(void) { return g_err.c_str(); }
 

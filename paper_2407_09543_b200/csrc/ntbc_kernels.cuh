@@ -394,6 +394,9 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     u = p.next_unit ? *next_slot : u + (int)gridDim.x * NWG;
   }
 
+  // the BC-word writers (lanes 0 and 16) order their stores at system scope before the kernel ends: the
+  // out pointers may be another GPU's memory mapped over NVLink (the fused peer gather, ntbc_peer_open)
+  if (!DUMP && (lane & 15) == 0) __threadfence_system();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem_base, NWG <= 2 ? 128 : NWG <= 4 ? 256 : 512);
 }

@@ -52,6 +52,9 @@ _SIGS = {
     "ntbc_debug_features": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ntbc_pack": (_i, [_i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "ntbc_debug_mma": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp]),
+    "ntbc_peer_export": (_i, [_vp, _vp]),
+    "ntbc_peer_open": (_i, [_vp, _i, C.POINTER(_vp)]),
+    "ntbc_peer_close": (_i, [_vp]),
     "ntbc_launch_count": (C.c_uint64, []),
     "ntbc_last_error": (C.c_char_p, []),
 }
@@ -131,9 +134,16 @@ def alloc_outputs(models, width: int, height: int, row_begin: int = 0, row_end: 
 
 
 def decode_material(models, width: int, height: int, outs=None, row_begin: int = 0, row_end: int | None = None,
-                    stream=None):
-    """ntbc_decode_material: returns one int64 [rows][W/4] tensor of BC words per texture."""
+                    stream=None, out_ptrs=None):
+    """ntbc_decode_material: returns one int64 [rows][W/4] tensor of BC words per texture.
+    out_ptrs: raw device pointers (one per texture) instead of tensors, e.g. rank 0's buffer mapped
+    with peer_open (the fused peer-memory gather); then nothing is returned."""
     row_end = height // 4 if row_end is None else row_end
+    if out_ptrs is not None:
+        ptrs = (_vp * len(out_ptrs))(*out_ptrs)
+        _check(_lib.ntbc_decode_material(_handles(models), len(models), width, height, row_begin, row_end, ptrs,
+                                         _stream(stream)))
+        return None
     if outs is None:
         outs = alloc_outputs(models, width, height, row_begin, row_end)
     ptrs = (_vp * len(outs))(*[o.data_ptr() for o in outs])
@@ -272,6 +282,29 @@ def debug_mma(A: torch.Tensor, B: torch.Tensor, Cin, K: int, N: int, stream=None
     D = torch.empty((128, N), dtype=torch.float32, device=A.device)
     _check(_lib.ntbc_debug_mma(A.data_ptr(), B.data_ptr(), _ptr(Cin), D.data_ptr(), K, N, _stream(stream)))
     return D
+
+
+PEER_HANDLE_BYTES = 72
+
+
+def peer_export(t: torch.Tensor) -> bytes:
+    """ntbc_peer_export: CUDA-IPC handle (+ offset) of a device tensor's memory, to send to other ranks."""
+    buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+    _check(_lib.ntbc_peer_export(t.data_ptr(), buf))
+    return buf.raw
+
+
+def peer_open(handle: bytes, device: int) -> int:
+    """ntbc_peer_open: map another process's exported memory on `device`; returns a raw device pointer."""
+    if len(handle) != PEER_HANDLE_BYTES:
+        raise ValueError("bad peer handle")
+    p = _vp()
+    _check(_lib.ntbc_peer_open(C.create_string_buffer(handle, PEER_HANDLE_BYTES), device, C.byref(p)))
+    return p.value
+
+
+def peer_close(ptr: int):
+    _check(_lib.ntbc_peer_close(ptr))
 
 
 def launch_count() -> int:

@@ -3,8 +3,12 @@
 Every BC word depends only on the model and its block coordinates, so the path shards with no
 data-path exchange: block-row ranges of one material (latency view) or whole materials of a batch
 (throughput view).  The only collective is the final gather of packed BC words to rank 0, which
-BASELINE.json's north star counts in the timing.  These helpers are backend-agnostic (NCCL on GPU
-tensors, gloo on CPU tensors for the tests).
+BASELINE.json's north star counts in the timing.  Two implementations:
+  * PeerGather (default on GPUs): the gather is fused into the decode -- every rank's fused kernel
+    stores its BC words straight into rank 0's buffer through a CUDA-IPC mapping (NVLink), unit by
+    unit while later units are computed; a one-element all-reduce then marks completion;
+  * gather_rows / gather_materials: a separate collective (dist.gather) after the decode -- NCCL on
+    GPU tensors, gloo on CPU tensors for the tests.
 """
 from __future__ import annotations
 
@@ -56,3 +60,44 @@ def gather_materials(local: torch.Tensor, rank: int, world: int, group=None):
     bufs = [torch.empty_like(local) for _ in range(world)] if rank == 0 else None
     dist.gather(local, bufs, dst=0, group=group)
     return bufs if rank == 0 else None
+
+
+class PeerGather:
+    """Fused gather of one [n_tex, BH, BW] material per rank into rank 0's [world, n_tex, BH, BW] buffer.
+
+    Rank 0 allocates the buffer and exports it (ntbc_peer_export); the handle is broadcast with the
+    process group; every other rank maps it (ntbc_peer_open) and decodes straight into its slice
+    (ntbc.decode_material(..., out_ptrs=self.ptrs)).  `complete()` is the only exchange on the timed
+    path: a one-element all-reduce ordered after the decode on every rank, after which rank 0's
+    buffer holds all materials (the writes are system-scope fenced by the fused kernel)."""
+
+    def __init__(self, n_tex: int, bh: int, bw: int, rank: int, world: int, device: torch.device, group=None):
+        from . import ntbc   # CUDA only; the CPU helpers above do not need the library
+        self.rank, self.world, self.group, self._opened = rank, world, group, None
+        self.buf = (torch.empty((world, n_tex, bh, bw), dtype=torch.int64, device=device) if rank == 0 else None)
+        obj = [ntbc.peer_export(self.buf) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        if rank == 0:
+            base = self.buf.data_ptr()
+        else:
+            base = self._opened = ntbc.peer_open(obj[0], device.index)
+        plane = bh * bw * 8
+        self.ptrs = [base + (rank * n_tex + k) * plane for k in range(n_tex)]
+        self._flag = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def complete(self):
+        """All ranks' decodes (issued before this call on the current stream) have landed in rank 0's buffer
+        once this all-reduce completes; the current stream waits for it (NCCL).  With a CPU backend (gloo,
+        the single-GPU functional test) the host synchronises the device and then joins a barrier."""
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    def close(self):
+        if self._opened is not None:
+            from . import ntbc
+            torch.cuda.synchronize()
+            ntbc.peer_close(self._opened)
+            self._opened = None

@@ -198,6 +198,10 @@ def run_ours(args, rank, world, local_rank):
     # NTBC_GATHER=nccl uses a separate NCCL gather after the decode instead
     gather_mode = os.environ.get("NTBC_GATHER", "peer") if world > 1 else "none"
     pg = PeerGather(n_tex, BH, BW, rank, world, dev) if gather_mode == "peer" else None
+    if pg is not None and not pg.ok:   # no IPC / peer access on this system: all ranks fall back together
+        print(f"rank {rank}: peer gather unavailable ({pg.error}); using the NCCL gather", file=sys.stderr)
+        pg.close()
+        pg, gather_mode = None, "nccl"
 
     def step():
         if pg is not None:

@@ -74,15 +74,32 @@ class PeerGather:
     def __init__(self, n_tex: int, bh: int, bw: int, rank: int, world: int, device: torch.device, group=None):
         from . import ntbc   # CUDA only; the CPU helpers above do not need the library
         self.rank, self.world, self.group, self._opened = rank, world, group, None
-        self.buf = (torch.empty((world, n_tex, bh, bw), dtype=torch.int64, device=device) if rank == 0 else None)
-        obj = [ntbc.peer_export(self.buf) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0, group=group)
+        self.buf, self.ptrs, self.error = None, None, None
+        handle = None
         if rank == 0:
-            base = self.buf.data_ptr()
-        else:
-            base = self._opened = ntbc.peer_open(obj[0], device.index)
-        plane = bh * bw * 8
-        self.ptrs = [base + (rank * n_tex + k) * plane for k in range(n_tex)]
+            try:
+                self.buf = torch.empty((world, n_tex, bh, bw), dtype=torch.int64, device=device)
+                handle = ntbc.peer_export(self.buf)
+            except Exception as e:   # e.g. an allocator without IPC support
+                self.error = f"export: {e}"
+        obj = [handle]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        base = None
+        if rank == 0:
+            base = self.buf.data_ptr() if handle is not None else None
+        elif obj[0] is not None:
+            try:
+                base = self._opened = ntbc.peer_open(obj[0], device.index)
+            except Exception as e:   # no peer access between these GPUs
+                self.error = f"open: {e}"
+        # every rank must agree, or the ranks would run different exchanges
+        ok = torch.tensor([1 if base is not None else 0], dtype=torch.int32,
+                          device=device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        self.ok = bool(ok.item())
+        if self.ok:
+            plane = bh * bw * 8
+            self.ptrs = [base + (rank * n_tex + k) * plane for k in range(n_tex)]
         self._flag = torch.zeros(1, dtype=torch.int32, device=device)
 
     def complete(self):

@@ -849,9 +849,18 @@ ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const 
     co += fmts[k] == NTBC_BC1 ? 3 : 1;
   }
   p.n_e = eo; p.n_c = co;
-  const long long pairs = (long long)((p.BW + 1) / 2) * p.rows;
-  const int grid = (int)std::min<long long>((pairs + 7) / 8, 148 * 8);
-  pack_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(p);
+  p.tiles_per_row = (p.BW + kPackTileBlocks - 1) / kPackTileBlocks;
+  p.n_tiles = p.tiles_per_row * p.rows;
+  const size_t smem = (384 + 4 * (4 * kPackTileBlocks * p.n_c + 4) + kPackTileBlocks * p.n_e) * sizeof(float) +
+                      kPackTileBlocks * kMaxTex * sizeof(uint32_t);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_kernel, 256, smem));
+  // persistent grid: exactly the resident CTAs (a second partial wave of grid-stride CTAs would double
+  // the tail), each striding over 16-block tiles
+  const int grid = std::max(1, std::min(p.n_tiles, sms * std::max(per_sm, 1)));
+  pack_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(p);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return NTBC_OK;

@@ -405,45 +405,85 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
 struct PackParams {
   const float* ep;   // [rows][BW][N_e]
   const float* col;  // [rows*4][W][N_c]
-  int W, BW, rows, n_e, n_c, n_tex;
+  int W, BW, rows, n_e, n_c, n_tex, tiles_per_row, n_tiles;
   int fmt[kMaxTex], ep_off[kMaxTex], col_off[kMaxTex];
   uint64_t* out[kMaxTex];
 };
-// one warp = two horizontally adjacent blocks; lane = texel (lane & 15) of block (lane >> 4)
+constexpr int kPackTileBlocks = 16;   // block positions per tile (one block row): 64 texel columns x 4 rows
+
+// Per tile: the tile's fp32 MLP outputs (4 texel rows x 64 texels x N_c, and 16 x N_e) are staged in
+// shared memory with coalesced 16-B loads (the only HBM traffic besides the BC words: every input byte
+// is read once); one thread per (block, texture) quantizes the endpoints into the BC word header (R11-R13);
+// then one warp per two blocks, lane = texel, rebuilds each palette from its header and the exact UNORM
+// tables, selects indices and packs the words as in the fused kernel's epilogue.
+__device__ __forceinline__ void pack_stage(float* dst, const float* src, int n) {
+  if ((((uintptr_t)src) & 15) == 0 && (n & 3) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int i = threadIdx.x; i < n / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+}
+
 __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams p) {
-  const int lane = threadIdx.x & 31;
-  const int pairs_per_row = (p.BW + 1) / 2;
-  const long long n_pairs = (long long)pairs_per_row * p.rows;
-  for (long long w = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < n_pairs;
-       w += (long long)gridDim.x * (blockDim.x / 32)) {
-    const int row = (int)(w / pairs_per_row);
-    const int bx = (int)(w % pairs_per_row) * 2 + (lane >> 4);
-    const bool valid = bx < p.BW;
-    const int bxc = valid ? bx : p.BW - 1;
-    const int i = lane & 15, x = 4 * bxc + (i & 3), y = 4 * row + (i >> 2);
-    const float* e = p.ep + ((size_t)row * p.BW + bxc) * p.n_e;
-    const float* c = p.col + ((size_t)y * p.W + x) * p.n_c;
-    for (int k = 0; k < p.n_tex; k++) {
-      uint64_t word;
+  extern __shared__ __align__(16) float psm[];
+  float* s_unorm = psm;                                   // 352 UNORM quotients + 32 BC4 weights
+  const int rs = 4 * kPackTileBlocks * p.n_c + 4;         // texel-row stride (+4 floats: rows start 4 banks apart)
+  float* s_col = psm + 384;                               // [4][64 * N_c + 4]
+  float* s_ep = s_col + 4 * rs;                           // [16][N_e]
+  uint32_t* s_hdr = reinterpret_cast<uint32_t*>(s_ep + kPackTileBlocks * p.n_e);   // [16][n_tex]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 352; i += blockDim.x)
+    s_unorm[i] = i < 32 ? __fdiv_rn((float)i, 31.0f) : i < 96 ? __fdiv_rn((float)(i - 32), 63.0f)
+                                                            : __fdiv_rn((float)(i - 96), 255.0f);
+  if (tid < 32) s_unorm[352 + tid] = bc4_weight(tid);
+  for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+    const int row = t / p.tiles_per_row, bx0 = (t - row * p.tiles_per_row) * kPackTileBlocks;
+    const int nb = min(kPackTileBlocks, p.BW - bx0);
+    __syncthreads();   // previous tile's readers are done (and the tables are written)
+    for (int yi = 0; yi < 4; yi++)
+      pack_stage(s_col + yi * rs, p.col + ((size_t)(4 * row + yi) * p.W + 4 * bx0) * p.n_c,
+                 4 * nb * p.n_c);
+    pack_stage(s_ep, p.ep + ((size_t)row * p.BW + bx0) * p.n_e, nb * p.n_e);
+    __syncthreads();
+    if (tid < nb * p.n_tex) {   // BC word headers: quantized endpoints (R11-R13)
+      const int b = tid / p.n_tex, k = tid - b * p.n_tex;
+      const float* e = s_ep + b * p.n_e + p.ep_off[k];
       if (p.fmt[k] == kFmtBC1) {
-        float ep[6], e0[3], e1[3];
+        float ep6[6];
 #pragma unroll
-        for (int q = 0; q < 6; q++) ep[q] = __ldg(e + p.ep_off[k] + q);
-        const uint32_t hdr = quant_bc1(ep, e0, e1);
-        const float cc[3] = {__ldg(c + p.col_off[k]), __ldg(c + p.col_off[k] + 1), __ldg(c + p.col_off[k] + 2)};
-        const uint32_t code = bc1_code(cc, e0, e1, (hdr & 0xFFFFu) == (hdr >> 16));
-        word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
+        for (int c = 0; c < 6; c++) ep6[c] = e[c];
+        bool swapped;
+        s_hdr[b * kMaxTex + k] = quant_bc1_hdr(ep6, swapped);
       } else {
-        float ep[2], e0, e1;
-        ep[0] = __ldg(e + p.ep_off[k]);
-        ep[1] = __ldg(e + p.ep_off[k] + 1);
-        const uint32_t hdr = quant_bc4(ep, e0, e1);
-        float pl[8];
-        bc4_palette(hdr, pl);
-        const uint32_t code = bc4_code(__ldg(c + p.col_off[k]), pl, (hdr & 0xFFu) > (hdr >> 8));
-        word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
+        const float ep2[2] = {e[0], e[1]};
+        s_hdr[b * kMaxTex + k] = quant_bc4_hdr(ep2);
       }
-      if ((lane & 15) == 0 && valid) p.out[k][(size_t)row * p.BW + bx] = word;
+    }
+    __syncthreads();
+    for (int wb = 2 * warp; wb < nb; wb += 2 * (blockDim.x >> 5)) {   // warp = blocks wb, wb + 1
+      const int h = lane >> 4, i = lane & 15, b = min(wb + h, nb - 1);
+      const bool valid = wb + h < nb;
+      const float* c = s_col + (i >> 2) * rs + (4 * b + (i & 3)) * p.n_c;
+      for (int k = 0; k < p.n_tex; k++) {
+        const uint32_t hdr = s_hdr[b * kMaxTex + k];
+        const int co = p.col_off[k];
+        uint64_t word;
+        if (p.fmt[k] == kFmtBC1) {
+          const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
+          const float e0[3] = {s_unorm[c0 >> 11], s_unorm[32 + ((c0 >> 5) & 63)], s_unorm[c0 & 31]};
+          const float e1[3] = {s_unorm[c1 >> 11], s_unorm[32 + ((c1 >> 5) & 63)], s_unorm[c1 & 31]};
+          const float cc[3] = {c[co], c[co + 1], c[co + 2]};
+          word = (uint64_t)hdr | (pack_bc1_indices(bc1_code(cc, e0, e1, c0 == c1), lane) << 32);
+        } else {
+          const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
+          float pl[8];
+          bc4_palette_tab(s_unorm[96 + E0], s_unorm[96 + E1], E0 > E1, s_unorm + 352, pl);
+          word = (uint64_t)hdr | (pack_bc4_indices(bc4_code(c[co], pl, E0 > E1), lane) << 16);
+        }
+        if ((lane & 15) == 0 && valid) p.out[k][(size_t)row * p.BW + bx0 + wb + h] = word;
+      }
     }
   }
 }

@@ -1,0 +1,62 @@
+"""Standalone pack kernel (rows a5-a8, ntbc_pack) on the C3 material: achieved HBM bandwidth.
+
+The fp32 MLP outputs of the whole 4096^2 C3 material (endpoints [1024][1024][18], colours
+[4096][4096][9]: 680 MB, produced once by ntbc_debug_mlp) are quantized, palettised, index-selected
+and packed into the 5 BC planes (40 MiB).  Algorithmic bytes per launch = inputs read once + BC words
+written once; achieved GB/s = those bytes / CUDA-event time (inputs 5x larger than L2, L2 also
+flushed between launches).  Writes profiles/pack_<tag>.json.
+
+usage: python tools/pack_bench.py [tag] [steps]
+"""
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from paper_2407_09543_b200 import ntbc  # noqa: E402
+
+
+def main(tag="r01", steps=20):
+    cfg = 3
+    W, H, spec = synth.config_shape(cfg)
+    m = ntbc.Model(synth.model_blob(cfg))
+    ep, col = ntbc.debug_mlp(m, W, H)
+    torch.cuda.synchronize()
+    outs = [torch.empty((H // 4, W // 4), dtype=torch.int64, device="cuda") for _ in m.fmts]
+    ref = ntbc.decode_material([m], W, H)   # the fused kernel's words: the pack kernel must agree
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        ntbc.pack(m.fmts, ep, col, W, H, outs=outs, stream=s)
+    torch.cuda.synchronize()
+    same = all(torch.equal(a, b) for a, b in zip(outs, ref))
+    ts = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        ntbc.pack(m.fmts, ep, col, W, H, outs=outs, stream=s)
+        b.record(s)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    ms = ts[len(ts) // 2]
+    nbytes = ep.numel() * 4 + col.numel() * 4 + sum(o.numel() * 8 for o in outs)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    out = {"kernel": "pack_kernel (ntbc_pack, rows a5-a8)", "config": "C3 4096^2, 2 BC1 + 3 BC4",
+           "algorithmic_bytes": nbytes, "median_ms": ms, "min_ms": ts[0], "achieved_gbs": gbs,
+           "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)",
+           "words_equal_fused_kernel": same}
+    print(json.dumps(out))
+    with open(os.path.join(ROOT, "profiles", f"pack_{tag}.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main(*(sys.argv[1:2] or []), *(int(x) for x in sys.argv[2:3]))

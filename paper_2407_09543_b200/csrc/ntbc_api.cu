@@ -52,6 +52,8 @@ struct Arch {
   int levels[2], coarsest[2];
   int dims[2][5];                 // [net][layer boundary]
   size_t level_off[2][kMaxLevels];
+  size_t fg_off[2][kMaxLevels];   // dequantized fp32 grid: level offsets inside that region
+  size_t fg_zero_off, fg_bytes;   // zero block read by the unused levels; region size
   float s[2][kMaxLevels];
   int z[2][kMaxLevels];
   size_t w_off[2][4], b_off[2][4];
@@ -102,13 +104,20 @@ ntbc_status parse(const void* blob, size_t n, Arch& a) {
       memcpy(&a.s[g][l], b + qp + 8 * li, 4);
       memcpy(&a.z[g][l], b + qp + 8 * li + 4, 4);
     }
-  for (int g = 0; g < 2; g++)
+  size_t fo = 0, zmax = 0;
+  for (int g = 0; g < 2; g++) {
     for (int l = 0; l < a.levels[g]; l++) {
       const size_t res = (size_t)a.coarsest[g] << l, sz = res * res * 2;
       a.level_off[g][l] = off;
       off += al16(sz);
       if (off > n + 15) return fail(NTBC_EFORMAT, "blob truncated in grid %d level %d", g, l);
+      a.fg_off[g][l] = fo;
+      fo += al16(sz * sizeof(float));
     }
+    zmax = std::max(zmax, (size_t)a.coarsest[g] * a.coarsest[g] * 2 * sizeof(float));
+  }
+  a.fg_zero_off = fo;
+  a.fg_bytes = fo + al16(zmax);
   const int ins[2] = {ep_in, col_in}, outs[2] = {n_e, n_c};
   for (int k = 0; k < 2; k++) {
     a.dims[k][0] = ins[k];
@@ -147,8 +156,9 @@ constexpr int kCopyStreams = 4;
 struct ntbc_model_s {
   int device;
   Arch arch;
-  uint8_t* d_blob = nullptr;   // device copy of the whole blob (grid payloads read in place)
-  size_t blob_cap = 0;
+  uint8_t* d_blob = nullptr;   // weight slot: the blob, then at fg_base its grids dequantized to fp32
+  size_t blob_cap = 0;         // slot bytes
+  size_t fg_base = 0;          // offset of the fp32 grids in a slot
   // dynamic-scheduling unit counters: a ring of kSchedRing ints, one per launch (zeroed on the
   // launch's stream), so up to kSchedRing launches of this model may be in flight concurrently
   int* d_sched = nullptr;
@@ -203,9 +213,35 @@ void layout_nets(ntbc_model_s* m) {
   }
 }
 
-// the whole model is the blob: one host->device copy into the current weight slot
+// the model is the blob: one host->device copy into the current weight slot
 ntbc_status upload(ntbc_model_s* m, const void* blob, size_t n, cudaStream_t st) {
   CUDA_TRY(cudaMemcpyAsync(m->d_blob, blob, n, cudaMemcpyHostToDevice, st));
+  return NTBC_OK;
+}
+
+// row a2, first half, at the start of every decode: one kernel dequantizes every grid level of the current
+// weight slot (Eq.2, R6) into the slot's fp32 grid region (and zeroes its zero block); the fused kernel
+// that follows on the same stream only interpolates
+ntbc_status dequant_grids(ntbc_model_s* m, cudaStream_t st) {
+  const Arch& a = m->arch;
+  DequantParams d{};
+  d.slot = m->d_blob;
+  for (int g = 0; g < 2; g++)
+    for (int l = 0; l < a.levels[g]; l++, d.n_levels++) {
+      const long long res = (long long)a.coarsest[g] << l;
+      d.src_off[d.n_levels] = a.level_off[g][l];
+      d.dst_off[d.n_levels] = m->fg_base + a.fg_off[g][l];
+      d.end[d.n_levels] = (d.n_levels ? d.end[d.n_levels - 1] : 0) + res * res * 2;
+      d.s[d.n_levels] = a.s[g][l];
+      d.z[d.n_levels] = a.z[g][l];
+    }
+  d.zero_off = m->fg_base + a.fg_zero_off;
+  d.zero_n = (int)((a.fg_bytes - a.fg_zero_off) / sizeof(float));
+  const long long total4 = d.end[d.n_levels - 1] / 4;
+  const int grid = (int)std::min<long long>((total4 + 255) / 256, 148 * 8);
+  dequant_grids_kernel<<<grid, 256, 0, st>>>(d);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
   return NTBC_OK;
 }
 
@@ -236,6 +272,8 @@ size_t fused_smem(const FusedParams& p, int nwg) {
 
 ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
   const Arch& a = m->arch;
+  ntbc_status dst = dequant_grids(m, st);
+  if (dst) return dst;
   if (!dump && m->d_sched && !(getenv("NTBC_STATIC_SCHED") && atoi(getenv("NTBC_STATIC_SCHED")))) {
     p.next_unit = m->d_sched + (m->sched_next++ % kSchedRing);
     CUDA_TRY(cudaMemsetAsync(p.next_unit, 0, sizeof(int), st));
@@ -244,16 +282,16 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
   for (int g = 0; g < 2; g++) {
     p.levels[g] = a.levels[g];
     for (int l = 0; l < a.levels[g]; l++) {
-      p.lv[g][l].offset = (uint32_t)a.level_off[g][l];
+      p.lv[g][l].offset = (uint32_t)(m->fg_base + a.fg_off[g][l]);
       p.lv[g][l].res = a.coarsest[g] << l;
       p.lv[g][l].s = a.s[g][l];
       p.lv[g][l].z = a.z[g][l];
     }
-    // levels past the grid's count read level 0 with s = 0, z = 0: the lookup then yields exactly +0
-    // (s*d = +-0, every lerp of signed zeros is +0), the zero feature the architecture defines, so
+    // levels past the grid's count read the slot's zero block at the coarsest resolution: the lookup
+    // then yields exactly +0 (every lerp of +0 is +0), the zero feature the architecture defines, so
     // the kernel samples all kMaxLevels levels without branches and can batch their loads.
     for (int l = a.levels[g]; l < kMaxLevels; l++) {
-      p.lv[g][l].offset = (uint32_t)a.level_off[g][0];
+      p.lv[g][l].offset = (uint32_t)(m->fg_base + a.fg_zero_off);
       p.lv[g][l].res = a.coarsest[g];
       p.lv[g][l].s = 0.0f;
       p.lv[g][l].z = 0;
@@ -415,12 +453,13 @@ ntbc_status ntbc_load_model(const void* blob, size_t nbytes, int cuda_device, nt
   m->device = cuda_device;
   m->arch = a;
   layout_nets(m);
-  if (cudaMalloc(&m->d_blob, al16(nbytes)) != cudaSuccess) {
+  m->fg_base = (al16(nbytes) + 255) & ~size_t(255);
+  m->blob_cap = m->fg_base + a.fg_bytes;
+  if (cudaMalloc(&m->d_blob, m->blob_cap) != cudaSuccess) {
     cudaGetLastError();
     ntbc_free_model(m);
-    return fail(NTBC_ENOMEM, "device allocation of %zu bytes failed", nbytes);
+    return fail(NTBC_ENOMEM, "device allocation of %zu bytes failed", m->blob_cap);
   }
-  m->blob_cap = al16(nbytes);
   if (cudaMalloc(&m->d_sched, kSchedRing * sizeof(int)) != cudaSuccess) { cudaGetLastError(); m->d_sched = nullptr; }
   st = upload(m, blob, nbytes, 0);
   if (st == NTBC_OK && cudaDeviceSynchronize() != cudaSuccess) st = fail(NTBC_ECUDA, "model upload: %s", cudaGetErrorString(cudaGetLastError()));

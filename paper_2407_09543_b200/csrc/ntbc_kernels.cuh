@@ -55,38 +55,52 @@ struct FusedParams {
   int naive;                    // 1: the texel net outputs one weight per texture (naive approach)
 };
 
+// ---------------------------------------------------------------- a2 at model upload: Eq.2 dequantization
+// Every grid level's uint8 codes become fp32 values v = RN(s (q - z)) (Eq.2; R6: one binary32
+// multiply of the exact integer q - z), stored [res][res][2] in the weight slot after the blob, once per
+// upload.  The decode kernel then reads 8-byte (f0, f1) vertices and only interpolates.
+struct DequantParams {
+  uint8_t* slot;                    // weight slot: blob at 0, fp32 grids at dst_off
+  int n_levels;                     // block-grid levels then texel-grid levels (<= 2 x kMaxLevels)
+  unsigned long long src_off[2 * kMaxLevels], dst_off[2 * kMaxLevels];
+  long long end[2 * kMaxLevels];    // cumulative code count (res^2 x 2) through level i
+  float s[2 * kMaxLevels];
+  int z[2 * kMaxLevels];
+  unsigned long long zero_off;      // zero block (unused levels read it)
+  int zero_n;
+};
+// four codes per thread (level sizes res^2 x 2 and all offsets are multiples of 16 bytes): one 4-byte
+// load, one 16-byte store
+__global__ void __launch_bounds__(256) dequant_grids_kernel(const __grid_constant__ DequantParams d) {
+  const long long total4 = d.end[d.n_levels - 1] / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += (long long)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (4 * i >= d.end[l]) l++;
+    const long long j = i - (l ? d.end[l - 1] / 4 : 0);
+    const uint32_t q4 = __ldg(reinterpret_cast<const uint32_t*>(d.slot + d.src_off[l]) + j);
+    const float s = d.s[l];
+    const int z = d.z[l];
+    reinterpret_cast<float4*>(d.slot + d.dst_off[l])[j] =
+        make_float4(__fmul_rn(s, (float)((int)(q4 & 0xFFu) - z)), __fmul_rn(s, (float)((int)((q4 >> 8) & 0xFFu) - z)),
+                    __fmul_rn(s, (float)((int)((q4 >> 16) & 0xFFu) - z)), __fmul_rn(s, (float)((int)(q4 >> 24) - z)));
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.zero_n; i += gridDim.x * blockDim.x)
+    reinterpret_cast<float*>(d.slot + d.zero_off)[i] = 0.0f;
+}
+
 // ---------------------------------------------------------------- a1-a2: coordinates + grid encode
-// Vertex-centred bilinear lookup of one level (R1), Eq.2 dequantization (R6), lerp = fma(t, b-a, a).
-// Both features of a vertex are processed as one fp32x2 pair.  (float)(q - z) is formed exactly as
-// (2^23 + q) - (2^23 + z) from a PRMT-assembled float (Sterbenz), identical to the integer conversion.
+// Vertex-centred bilinear lookup of one level (R1) of the dequantized grid (R6), lerp = fma(t, b-a, a),
+// both features of a vertex as one fp32x2 pair (one 8-byte load per vertex).
 // The reading's clamp i0 = min(floor(X), res-2) never binds here: callers pass p in (0, 1) (rows past
 // the texture edge are clamped to the last valid block/texel), so X = RN(p (res-1)) < res - 1.
-// NOTE: ptxas contracts a mul.rn.f32x2 feeding an add/sub.rn.f32x2 into FFMA2 even with --fmad=false
-// (verified with cuobjdump), which would change the rounding.  Every product that feeds an addition is
-// therefore a scalar __fmul_rn (scalar FMUL -> FADD2 is never contracted); only the lerps are packed.
 __device__ __forceinline__ uint64_t level_lookup2(const uint8_t* blob, const GridLevel& L, float pu, float pv) {
   const float rm1 = (float)(L.res - 1);
   const float X = __fmul_rn(pu, rm1), Y = __fmul_rn(pv, rm1);
   const int i0 = __float2int_rd(X), j0 = __float2int_rd(Y);
   float fx, fy;
   f2unpack(sub2(f2pack(X, Y), f2pack((float)i0, (float)j0)), fx, fy);
-  const uint16_t* g = reinterpret_cast<const uint16_t*>(blob + L.offset) + (j0 * L.res + i0);
-  const uint32_t q00 = __ldg(g), q10 = __ldg(g + 1), q01 = __ldg(g + L.res), q11 = __ldg(g + L.res + 1);
-  const float zf = __int_as_float(0x4B000000 + L.z);  // 2^23 + z (z in [0, 255])
-  const uint64_t Z2 = f2pack(zf, zf);
-  float d[8];
-  f2unpack(sub2(f2pack(__int_as_float(__byte_perm(q00, 0x4B000000u, 0x7540)),
-                       __int_as_float(__byte_perm(q00, 0x4B000000u, 0x7541))), Z2), d[0], d[1]);
-  f2unpack(sub2(f2pack(__int_as_float(__byte_perm(q10, 0x4B000000u, 0x7540)),
-                       __int_as_float(__byte_perm(q10, 0x4B000000u, 0x7541))), Z2), d[2], d[3]);
-  f2unpack(sub2(f2pack(__int_as_float(__byte_perm(q01, 0x4B000000u, 0x7540)),
-                       __int_as_float(__byte_perm(q01, 0x4B000000u, 0x7541))), Z2), d[4], d[5]);
-  f2unpack(sub2(f2pack(__int_as_float(__byte_perm(q11, 0x4B000000u, 0x7540)),
-                       __int_as_float(__byte_perm(q11, 0x4B000000u, 0x7541))), Z2), d[6], d[7]);
-  const uint64_t v00 = f2pack(__fmul_rn(L.s, d[0]), __fmul_rn(L.s, d[1]));
-  const uint64_t v10 = f2pack(__fmul_rn(L.s, d[2]), __fmul_rn(L.s, d[3]));
-  const uint64_t v01 = f2pack(__fmul_rn(L.s, d[4]), __fmul_rn(L.s, d[5]));
-  const uint64_t v11 = f2pack(__fmul_rn(L.s, d[6]), __fmul_rn(L.s, d[7]));
+  const unsigned long long* g = reinterpret_cast<const unsigned long long*>(blob + L.offset) + (j0 * L.res + i0);
+  const uint64_t v00 = __ldg(g), v10 = __ldg(g + 1), v01 = __ldg(g + L.res), v11 = __ldg(g + L.res + 1);
   const uint64_t FX = f2pack(fx, fx), FY = f2pack(fy, fy);
   const uint64_t top = fma2(FX, sub2(v10, v00), v00), bot = fma2(FX, sub2(v11, v01), v01);
   return fma2(FY, sub2(bot, top), top);

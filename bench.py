@@ -315,6 +315,8 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
                      "frac": achieved / alu_peak, "traffic": traffic,
                      "kernel": "fused_decode_kernel", "kernel_ms": k_ms,
+                     "kernel_ms_covers": "CUDA events around ntbc_decode_material: dequant_grids_kernel "
+                                         "(row a2's Eq.2 half, ~1% of the step) + fused_decode_kernel",
                      "ops_per_texel": per_texel, "ops_per_block": per_block,
                      "peak_source": f"{n_sm} SMs x 128 lane-instr/clk x {sm_max:.0f} MHz (DESIGN.md §7.3)",
                      "tensor": {"achieved_tflops": mma_flops_per_material(spec, W, H) / (k_ms * 1e-3) / 1e12,

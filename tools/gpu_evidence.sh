@@ -14,4 +14,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${tag}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_decode -c 1 -o gpurun_out/${tag} \
   python tools/profile_step.py 3 2 > gpurun_out/${tag}_ncu_full.log 2>&1
+python tools/tab1.py ${tag} 20 > gpurun_out/${tag}_tab1.log 2>&1; cp profiles/tab1_${tag}.json gpurun_out/
+python tools/pack_bench.py ${tag} 20 > gpurun_out/${tag}_pack.log 2>&1; cp profiles/pack_${tag}.json gpurun_out/
 ls -la gpurun_out

@@ -289,11 +289,14 @@ def run_ours(args, rank, world, local_rank):
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     alu_peak = n_sm * 128 * sm_max * 1e6 / 1e9          # Gop/s: 128 lane-instructions / clk / SM
     achieved = ops / (k_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, ncu_ctx = None, None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "latest_fused_traffic.json")))
         if prof.get("config") == args.config:
             traffic = prof.get("dram_bytes_per_launch")
+            # cross-check of the op-count fraction with hardware counters from the committed ncu capture
+            ncu_ctx = {k: prof.get(k) for k in ("source", "issue_active", "alu_pipe", "fma_pipe", "tensor_pipe",
+                                                 "thread_instructions_per_texel")}
     except Exception:
         pass
     cpu = None
@@ -317,7 +320,7 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": "fused_decode_kernel", "kernel_ms": k_ms,
                      "kernel_ms_covers": "CUDA events around ntbc_decode_material: dequant_grids_kernel "
                                          "(row a2's Eq.2 half, ~1% of the step) + fused_decode_kernel",
-                     "ops_per_texel": per_texel, "ops_per_block": per_block,
+                     "ops_per_texel": per_texel, "ops_per_block": per_block, "ncu": ncu_ctx,
                      "peak_source": f"{n_sm} SMs x 128 lane-instr/clk x {sm_max:.0f} MHz (DESIGN.md §7.3)",
                      "tensor": {"achieved_tflops": mma_flops_per_material(spec, W, H) / (k_ms * 1e-3) / 1e12,
                                 "peak_tflops": peaks.get("bf16_tflops", 1658.0),

@@ -68,7 +68,14 @@ def main(rep, tag, config=3, texels=4096 * 4096):
     with open(os.path.join(ROOT, "profiles", f"{tag}_fused_ncu.json"), "w") as f:
         json.dump(out, f, indent=1)
     with open(os.path.join(ROOT, "profiles", "latest_fused_traffic.json"), "w") as f:
-        json.dump({"config": config, "dram_bytes_per_launch": rd + wr, "source": f"{tag}_fused_ncu.json"}, f)
+        def pct(k):
+            return float(m[k][0]) / 100.0 if k in m else None
+        json.dump({"config": config, "dram_bytes_per_launch": rd + wr, "source": f"{tag}_fused_ncu.json",
+                   "issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                   "alu_pipe": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                   "fma_pipe": pct("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                   "tensor_pipe": pct("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "thread_instructions_per_texel": out.get("thread_instructions_per_texel")}, f)
     lines = [f"# ncu --set full summary: {out['kernel'][:90]}", "", f"report: `{rep}` (tag {tag})", "",
              "| metric | value |", "|---|---|"]
     for k in KEYS:

@@ -284,6 +284,7 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
     for (int l = 0; l < a.levels[g]; l++) {
       p.lv[g][l].offset = (uint32_t)(m->fg_base + a.fg_off[g][l]);
       p.lv[g][l].res = a.coarsest[g] << l;
+      p.lv[g][l].rm1 = (float)((a.coarsest[g] << l) - 1);
       p.lv[g][l].s = a.s[g][l];
       p.lv[g][l].z = a.z[g][l];
     }
@@ -293,6 +294,7 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
     for (int l = a.levels[g]; l < kMaxLevels; l++) {
       p.lv[g][l].offset = (uint32_t)(m->fg_base + a.fg_zero_off);
       p.lv[g][l].res = a.coarsest[g];
+      p.lv[g][l].rm1 = (float)(a.coarsest[g] - 1);
       p.lv[g][l].s = 0.0f;
       p.lv[g][l].z = 0;
     }

@@ -22,9 +22,10 @@ constexpr int kFmtBC1 = 1;
 constexpr int kUnormBytes = 1536;  // 352 fp32 UNORM expansion values (q/31, q/63, q/255) + 32 BC4 weights
 
 struct GridLevel {
-  uint32_t offset;  // byte offset of the level payload [res][res][2] in the model blob (device copy)
+  uint32_t offset;  // byte offset of the level's dequantized fp32 [res][res][2] in the weight slot
   int res;
-  float s;          // Eq.2 scale
+  float rm1;        // (float)(res - 1), the lattice scale of R1
+  float s;          // Eq.2 scale (applied by dequant_grids_kernel)
   int z;            // Eq.2 zero point
 };
 
@@ -94,8 +95,7 @@ __global__ void __launch_bounds__(256) dequant_grids_kernel(const __grid_constan
 // The reading's clamp i0 = min(floor(X), res-2) never binds here: callers pass p in (0, 1) (rows past
 // the texture edge are clamped to the last valid block/texel), so X = RN(p (res-1)) < res - 1.
 __device__ __forceinline__ uint64_t level_lookup2(const uint8_t* blob, const GridLevel& L, float pu, float pv) {
-  const float rm1 = (float)(L.res - 1);
-  const float X = __fmul_rn(pu, rm1), Y = __fmul_rn(pv, rm1);
+  const float X = __fmul_rn(pu, L.rm1), Y = __fmul_rn(pv, L.rm1);
   const int i0 = __float2int_rd(X), j0 = __float2int_rd(Y);
   float fx, fy;
   f2unpack(sub2(f2pack(X, Y), f2pack((float)i0, (float)j0)), fx, fy);

@@ -252,7 +252,8 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- end to end through the C ABI with host buffers (pinned blob in, pinned BC words out)
     pinned_blob = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
-    host_out = [torch.empty((BH, BW), dtype=torch.int64).pin_memory() for _ in range(n_tex)]
+    host_all = torch.empty((n_tex, BH, BW), dtype=torch.int64).pin_memory()   # one pinned [tex][BH][BW] buffer
+    host_out = [host_all[k] for k in range(n_tex)]
     for _ in range(2):
         ntbc.decode_material_host([model], [pinned_blob], W, H, host_out, stream=stream)
     torch.cuda.synchronize()

@@ -96,6 +96,9 @@ ntbc_status ntbc_decode_material(const ntbc_model* models, int n_models, int wid
  * previous call's kernel; the kernel publishes finished row chunks (1/16 of the rows each) through
  * device counters and an internal copy stream copies each chunk back while later rows are decoded.
  * `stream` waits for all of it, so host_out is complete once `stream` reaches this call.
+ * When host_out[t..] of a model are equally spaced planes inside one pinned allocation (e.g. views of a
+ * [tex][H/4][W/4] buffer), each chunk is one 2-D copy for all textures and the last quarter of the rows
+ * is copied in smaller chunks (a shorter exposed tail); otherwise one copy per texture and chunk.
  * Not re-entrant per model: calls on the same model must not run concurrently on different streams.
  * Errors: as ntbc_decode_material, plus NTBC_ENOMEM. */
 ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, const void* const* blobs,

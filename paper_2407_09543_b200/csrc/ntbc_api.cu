@@ -436,6 +436,25 @@ ntbc_status check_dims(int W, int H, int r0, int r1) {
 
 // ---------------------------------------------------------------- peer-memory gather plumbing (CUDA IPC)
 typedef CUresult (*addr_range_fn)(CUdeviceptr*, size_t*, CUdeviceptr);
+static addr_range_fn get_addr_range() {
+  static addr_range_fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<addr_range_fn>(f);
+  }();
+  return fn;
+}
+// [p, p + bytes) lies inside one CUDA allocation (device memory, or pinned host memory through its UVA address)
+static bool one_allocation(const void* p, size_t bytes) {
+  addr_range_fn fn = get_addr_range();
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (!fn || fn(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS) { cudaGetLastError(); return false; }
+  return (CUdeviceptr)p >= base && (CUdeviceptr)p + bytes <= base + size;
+}
 static std::mutex g_peer_mu;
 static std::unordered_map<void*, void*> g_peer_base;   // pointer returned by ntbc_peer_open -> mapped base
 
@@ -599,9 +618,30 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
     // rows finish last, and only the final chunk's copy is exposed after the kernel
     // 16 chunks (measured with the upload placed under the kernel: 4/8/16/32 chunks -> 2.67/2.60/2.57/
     // 2.59 ms per C3 call; each stream wait + its copies has a fixed cost, the last chunk is the tail)
+    // > 0 when host_out[t..t+n_tex) are planes at one fixed pitch inside ONE pinned allocation (e.g. views of a
+    // [tex][BH][BW] tensor): then one 2-D copy per chunk moves every texture (fewer, larger copies: the
+    // per-copy cost is what limits fine chunking)
+    size_t host_pitch = 0;
+    if (n_tex > 1) {
+      const ptrdiff_t d = (const uint8_t*)host_out[t + 1] - (const uint8_t*)host_out[t];
+      bool uniform = d >= (ptrdiff_t)plane;
+      for (int k = 2; k < n_tex && uniform; k++)
+        uniform = (const uint8_t*)host_out[t + k] - (const uint8_t*)host_out[t + k - 1] == d;
+      if (uniform && one_allocation(host_out[t], (size_t)d * (n_tex - 1) + plane)) host_pitch = (size_t)d;
+    }
+    // copy-back chunks: 1/16 of the rows each; with 2-D copies the last quarter in 1/64 chunks: the rows of the
+    // kernel's last wave of units finish only at its end, and the smaller the chunks they fall into, the less
+    // is copied after it (exposed tail 0.12 -> 0.06 ms).  With one copy per texture and chunk, the per-copy
+    // cost of the extra chunks outweighs that (measured 0.31 ms tail), so those stay uniform.
     const int big = std::max(1, (BH + 15) / 16);
-    const int n_chunks = (BH + big - 1) / big;
-    auto chunk_rows = [&](int c, int& r0, int& r1) { r0 = c * big; r1 = std::min(BH, r0 + big); };
+    const int tail_row0 = host_pitch ? std::min(BH, (3 * BH / 4) / big * big) : BH;
+    const int small = std::max(1, big / 4);
+    const int n_big = (tail_row0 + big - 1) / big;   // the last one partial when tail_row0 = BH is no multiple
+    const int n_chunks = n_big + (BH - tail_row0 + small - 1) / small;
+    auto chunk_rows = [&](int c, int& r0, int& r1) {
+      if (c < n_big) { r0 = c * big; r1 = std::min(tail_row0, r0 + big); }
+      else { r0 = tail_row0 + (c - n_big) * small; r1 = std::min(BH, r0 + small); }
+    };
     const bool pipelined = stream_waits_supported(m->device) && n_chunks <= kMaxChunks && ensure_copy_state(m);
     if (!pipelined) {
       st = ntbc_model_upload_async(m, blobs[i], blob_sizes[i], stream);
@@ -629,6 +669,8 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
     if (pipelined) {
       p.progress = m->d_progress;
       p.chunk_rows = big;
+      p.tail_row0 = tail_row0;
+      p.tail_rows = small;
     }
     const bool tl = pipelined && getenv("NTBC_TIMELINE") && atoi(getenv("NTBC_TIMELINE"));
     if (tl && !m->tlset[1][0])
@@ -660,9 +702,14 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
         if (!last && g_wait64((CUstream)xs, (CUdeviceptr)(m->d_progress + c), m->progress_target[c],
                               CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
           return fail(NTBC_ECUDA, "stream wait on progress counter failed");
-        for (int k = 0; k < n_tex; k++)
-          CUDA_TRY(cudaMemcpyAsync((uint8_t*)host_out[t + k] + r0 * row_bytes, (const uint8_t*)p.out[k] + r0 * row_bytes,
-                                   (size_t)(r1 - r0) * row_bytes, cudaMemcpyDeviceToHost, xs));
+        if (host_pitch)   // the caller's planes are equally spaced: one 2-D copy moves the chunk of every texture
+          CUDA_TRY(cudaMemcpy2DAsync((uint8_t*)host_out[t] + r0 * row_bytes, host_pitch,
+                                     (const uint8_t*)p.out[0] + r0 * row_bytes, plane, (size_t)(r1 - r0) * row_bytes,
+                                     n_tex, cudaMemcpyDeviceToHost, xs));
+        else
+          for (int k = 0; k < n_tex; k++)
+            CUDA_TRY(cudaMemcpyAsync((uint8_t*)host_out[t + k] + r0 * row_bytes, (const uint8_t*)p.out[k] + r0 * row_bytes,
+                                     (size_t)(r1 - r0) * row_bytes, cudaMemcpyDeviceToHost, xs));
       }
       for (int i = 0; i < kCopyStreams; i++) {   // the caller's stream sees every finished copy
         if (tl) CUDA_TRY(cudaEventRecord(m->tl[4 + i], m->copy_stream[i]));
@@ -930,14 +977,11 @@ ntbc_status ntbc_peer_export(const void* device_ptr, void* handle_out) {
   CUDA_TRY(cudaPointerGetAttributes(&at, device_ptr));
   if (at.type != cudaMemoryTypeDevice) return fail(NTBC_EINVAL, "not a device allocation");
   DevGuard dg(at.device);
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-      q != cudaDriverEntryPointSuccess || !fn)
-    return fail(NTBC_ECUDA, "cuMemGetAddressRange unavailable");
+  addr_range_fn fn = get_addr_range();
+  if (!fn) return fail(NTBC_ECUDA, "cuMemGetAddressRange unavailable");
   CUdeviceptr base = 0;
   size_t size = 0;
-  if (reinterpret_cast<addr_range_fn>(fn)(&base, &size, (CUdeviceptr)device_ptr) != CUDA_SUCCESS)
+  if (fn(&base, &size, (CUdeviceptr)device_ptr) != CUDA_SUCCESS)
     return fail(NTBC_ECUDA, "cuMemGetAddressRange failed");
   cudaIpcMemHandle_t h;
   CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base));

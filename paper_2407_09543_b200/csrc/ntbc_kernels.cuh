@@ -51,7 +51,8 @@ struct FusedParams {
   uint32_t a_bytes, pal_bytes;  // per-work-group shared memory regions
   uint32_t debug_flags;         // bit 1: grid-feature dump (ntbc_debug_features)
   unsigned long long* progress; // optional: per-chunk count of finished units (pipelined D2H, see ntbc_api.cu)
-  int chunk_rows;               // block rows per progress chunk
+  int chunk_rows;               // block rows per progress chunk before tail_row0 ...
+  int tail_row0, tail_rows;     // ... and per (smaller) chunk from tail_row0 on (local rows)
   int* next_unit;               // optional: dynamic unit counter (zeroed before the launch)
   int naive;                    // 1: the texel net outputs one weight per texture (naive approach)
 };
@@ -402,7 +403,9 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       if (r == 0) {
         __threadfence_system();   // the consumer is the copy engine (measured: same cost as a gpu fence)
         const int row = u / p.units_per_row;
-        atomicAdd(p.progress + row / p.chunk_rows, 1ull);
+        const int chunk = row < p.tail_row0 ? row / p.chunk_rows
+                                            : p.tail_row0 / p.chunk_rows + (row - p.tail_row0) / p.tail_rows;
+        atomicAdd(p.progress + chunk, 1ull);
       }
     }
     u = p.next_unit ? *next_slot : u + (int)gridDim.x * NWG;

@@ -329,16 +329,22 @@ def test_host_entry_point_matches_device_path(ntbc):
         assert np.array_equal(host[k].numpy().view(np.uint64)[:4], ref[k])
 
 
-@pytest.mark.parametrize("W,H", [(1024, 1024), (1000, 996), (64, 8)])
-def test_host_entry_point_pipelined_copies(ntbc, W, H):
+@pytest.mark.parametrize("W,H,contiguous", [(1024, 1024, False), (1000, 996, False), (64, 8, False),
+                                            (1024, 1024, True), (1000, 996, True), (4096, 4096, True)])
+def test_host_entry_point_pipelined_copies(ntbc, W, H, contiguous):
     """ntbc_decode_material_host copies row chunks back while the kernel runs (progress counters,
     DESIGN.md §6): repeated calls with changing weights and ragged shapes must return every word of the
-    device path, and sampled rows (first / last of the texture) must equal the oracle."""
+    device path, and sampled rows (first / last of the texture) must equal the oracle.  contiguous: the
+    texture planes are views of one pinned [tex][BH][BW] buffer (one 2-D copy per chunk)."""
     m = ntbc.Model(synth.model_blob(2, material=0))
     for material in (1, 2, 1):
         blob = synth.model_blob(2, material=material)
         pinned = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
-        host = [torch.full((H // 4, W // 4), -1, dtype=torch.int64).pin_memory() for _ in range(m.n_tex)]
+        if contiguous:
+            whole = torch.full((m.n_tex, H // 4, W // 4), -1, dtype=torch.int64).pin_memory()
+            host = [whole[k] for k in range(m.n_tex)]
+        else:
+            host = [torch.full((H // 4, W // 4), -1, dtype=torch.int64).pin_memory() for _ in range(m.n_tex)]
         ntbc.decode_material_host([m], [pinned], W, H, host)
         torch.cuda.synchronize()
         dev = ntbc.decode_material([m], W, H)

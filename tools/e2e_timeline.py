@@ -15,7 +15,8 @@ W, H, _ = synth.config_shape(cfg)
 blob = synth.model_blob(cfg)
 m = ntbc.Model(blob)
 pinned = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
-host = [torch.empty((H // 4, W // 4), dtype=torch.int64).pin_memory() for _ in range(m.n_tex)]
+host_all = torch.empty((m.n_tex, H // 4, W // 4), dtype=torch.int64).pin_memory()
+host = [host_all[k] for k in range(m.n_tex)] if os.environ.get("NTBC_SEPARATE_PLANES") != "1" else [torch.empty((H // 4, W // 4), dtype=torch.int64).pin_memory() for _ in range(m.n_tex)]
 stream = torch.cuda.Stream()
 for _ in range(3):
     ntbc.decode_material_host([m], [pinned], W, H, host, stream=stream)

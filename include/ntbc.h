@@ -53,8 +53,9 @@ typedef struct {
 } ntbc_model_info;
 
 /* Parse and validate a host .ntbc blob (int8 grids + per-level (s, z) + fp16 MLPs,
- * PAPER.md:321-322, 342) and upload it to `cuda_device`: grids as-is, MLP weights re-laid-out into
- * the tcgen05 shared-memory operand layout with the bias folded in as an extra K chunk.
+ * PAPER.md:321-322, 342) and upload it to `cuda_device` as-is (one copy into a device weight slot that
+ * also holds the fp32 grid region every decode dequantizes into; the fused kernel builds the tcgen05
+ * shared-memory operand images of the MLPs, bias folded in as an extra K chunk, in its prologue).
  * The blob is not retained (caller may free it after return).  Synchronous.
  * Errors: NTBC_EINVAL (NULL args), NTBC_EFORMAT, NTBC_ENOMEM, NTBC_ECUDA. */
 ntbc_status ntbc_load_model(const void* blob, size_t nbytes, int cuda_device, ntbc_model* out);
@@ -68,8 +69,9 @@ ntbc_status ntbc_model_upload_async(ntbc_model m, const void* blob, size_t nbyte
 ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out);
 void ntbc_free_model(ntbc_model m);                     /* NULL ok; caller guarantees no in-flight use */
 
-/* Rows a1-a8 of SURVEY §8, one fused sm_100a kernel per model: grid dequant + bilinear sampling
- * (Eq.2), endpoint MLP per block and colour MLP per texel on tcgen05 tensor cores
+/* Rows a1-a8 of SURVEY §8, two launches per model: the grid dequantization (Eq.2; every level's
+ * codes -> fp32 in the model's weight slot), then one fused sm_100a kernel: bilinear sampling
+ * (P:334-337), endpoint MLP per block and colour MLP per texel on tcgen05 tensor cores
  * (P:257-272), endpoint quantization (R11-R13), palettes (Eq.7/8), per-texel
  * argmax of negative distance (Eq.9-10) and BC1/BC4 bit packing.
  *   models / n_models: 1 = aggressive (one model), 2 = conservative (an all-BC1 model and

@@ -37,7 +37,10 @@ def ops_per_material(spec, W, H):
     tensor-core contraction: one op per IEEE operation, integer op or conversion."""
     n_bc1 = sum(1 for f in spec.fmts if f == 1)
     n_bc4 = len(spec.fmts) - n_bc1
-    selu, sig, lvl = 18, 16, 48            # per hidden activation (incl. fp16 cvt), per sigmoid, per grid level (R9 v3)
+    # per hidden activation (incl. fp16 cvt, R9 v3), per sigmoid, per grid level and texel (coordinates, floor,
+    # fractions, index, 3 lerps x 2 features, fp16 cvt; the Eq.2 dequantization runs once per vertex in
+    # dequant_grids_kernel since r01w and is not counted per texel)
+    selu, sig, lvl = 18, 16, 22
     hidden = spec.hidden * spec.n_hidden
     per_texel = hidden * selu + spec.n_color_out * sig + spec.texel_levels * lvl + 4 + 46 * n_bc1 + 42 * n_bc4
     per_block = (hidden * selu + spec.n_endpoint_out * sig + spec.block_levels * lvl + 4 + 40 * n_bc1 + 12 * n_bc4)

@@ -211,14 +211,17 @@ def test_conservative_pair_and_mismatch_rules(ntbc):
         assert np.array_equal(u64(outs[k]), ref[k])
     with pytest.raises(ntbc.NtbcError):   # two all-BC1 models are not a conservative pair
         ntbc.decode_material([ms[0], ms[0]], W, H)
-    # the same pair through the pipelined host entry point (two models, two uploads, one call)
+    # the same pair through the pipelined host entry point (two models, two uploads, one call), with
+    # separate pinned planes (one copy per texture and chunk) and with views of one pinned buffer (2-D copies)
     pinned = [torch.frombuffer(bytearray(b), dtype=torch.uint8).pin_memory() for b in (rgb, sc)]
-    host = [torch.full((H // 4, W // 4), -1, dtype=torch.int64).pin_memory() for _ in range(6)]
-    for _ in range(2):
-        ntbc.decode_material_host(ms, pinned, W, H, host)
-        torch.cuda.synchronize()
-        for k in range(6):
-            assert np.array_equal(host[k].numpy().view(np.uint64), ref[k])
+    whole = torch.full((6, H // 4, W // 4), -1, dtype=torch.int64).pin_memory()
+    for host in ([torch.full((H // 4, W // 4), -1, dtype=torch.int64).pin_memory() for _ in range(6)],
+                 [whole[k] for k in range(6)]):
+        for _ in range(2):
+            ntbc.decode_material_host(ms, pinned, W, H, host)
+            torch.cuda.synchronize()
+            for k in range(6):
+                assert np.array_equal(host[k].numpy().view(np.uint64), ref[k])
 
 
 def test_naive_c1_full_material(ntbc):

@@ -135,8 +135,9 @@ ntbc_status ntbc_encode_bc(const float* texels, ntbc_format fmt, int width, int 
  * for the MLP) with step number `step` (>= 1).
  *   xy: device int32 [B][2] texel coordinates (< W, H); cref: device fp32 [B][N_c] reference colours
  *   (head order); eref: device fp32 [B][N_e] reference endpoints of each texel's block (BC1: e0 rgb,
- *   e1 rgb; BC4: e0, e1); loss: device fp32 scalar (overwritten).  Not deterministic in the last bits
- *   (atomic accumulation order).  Errors: NTBC_EINVAL, NTBC_ECUDA. */
+ *   e1 rgb; BC4: e0, e1); loss: device fp32 scalar (overwritten).  grads must be 16-B aligned (gradients
+ *   are accumulated with 8- and 16-byte vector atomics).  Not deterministic in the last bits (atomic
+ *   accumulation order).  Errors: NTBC_EINVAL, NTBC_ECUDA. */
 typedef struct {
   int n_textures, fmt[8], hidden, levels, coarsest;
   int qat;   /* 1: the grid passes the per-level 8-bit fake quantizer (Eq. 1-5; DESIGN R33) */

@@ -818,6 +818,7 @@ ntbc_status train_step(int net, const ntbc_train_arch* arch, float* params, floa
   const long long n = g_train_total, n_grid = p.w_off[0];
   if (!params || !grads || !adam_m || !adam_v || !xy || !cref || !eref || !loss) return fail(NTBC_EINVAL, "NULL argument");
   if (batch < 1 || width < 1 || height < 1 || step < 1 || !(temperature > 0.0f)) return fail(NTBC_EINVAL, "bad batch/size/step/T");
+  if ((uintptr_t)grads & 15) return fail(NTBC_EINVAL, "grads not 16-B aligned (vector atomics)");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaMemsetAsync(grads, 0, (size_t)n * sizeof(float), st));
   CUDA_TRY(cudaMemsetAsync(loss, 0, sizeof(float), st));

@@ -342,9 +342,9 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
           acc[1][2] = __fmaf_rn(a1, d.z, acc[1][2]); acc[1][3] = __fmaf_rn(a1, d.w, acc[1][3]);
         }
 #pragma unroll
-        for (int r = 0; r < 2; r++)
-#pragma unroll
-          for (int c = 0; c < 4; c++) atomicAdd(p.grads + p.w_off[l] + (size_t)(k + r) * N + j + c, acc[r][c]);
+        for (int r = 0; r < 2; r++)   // one 16-byte vector atomic per 4 consecutive weights (sm_90+)
+          atomicAdd(reinterpret_cast<float4*>(p.grads + p.w_off[l] + (size_t)(k + r) * N + j),
+                    make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
       }
     } else {
       for (int e = t; e < K * N; e += NT) {
@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
       float* g = p.grads + p.lvl_off[l];
       const float* gv = p.params + p.lvl_off[l];
       const size_t c00 = ((size_t)j0 * res + i0) * 2, c10 = c00 + 2, c01 = c00 + (size_t)res * 2, c11 = c01 + 2;
+      float v00[2], v10[2], v01[2], v11[2];
       for (int f = 0; f < 2; f++) {
         const float d = D[tid * LD + 2 * l + f];
         float m00, m10, m01, m11;   // QAT STE: no gradient through clamped values
@@ -406,11 +407,16 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
         fake_quant(gv[c10 + f], p.qsz, l, m10);
         fake_quant(gv[c01 + f], p.qsz, l, m01);
         fake_quant(gv[c11 + f], p.qsz, l, m11);
-        atomicAdd(g + c00 + f, m00 * d * (1.0f - fx) * (1.0f - fy));
-        atomicAdd(g + c10 + f, m10 * d * fx * (1.0f - fy));
-        atomicAdd(g + c01 + f, m01 * d * (1.0f - fx) * fy);
-        atomicAdd(g + c11 + f, m11 * d * fx * fy);
+        v00[f] = m00 * d * (1.0f - fx) * (1.0f - fy);
+        v10[f] = m10 * d * fx * (1.0f - fy);
+        v01[f] = m01 * d * (1.0f - fx) * fy;
+        v11[f] = m11 * d * fx * fy;
       }
+      // both features of a vertex with one 8-byte vector atomic (sm_90+): half the atomics of the scatter
+      atomicAdd(reinterpret_cast<float2*>(g + c00), make_float2(v00[0], v00[1]));
+      atomicAdd(reinterpret_cast<float2*>(g + c10), make_float2(v10[0], v10[1]));
+      atomicAdd(reinterpret_cast<float2*>(g + c01), make_float2(v01[0], v01[1]));
+      atomicAdd(reinterpret_cast<float2*>(g + c11), make_float2(v11[0], v11[1]));
     }
   }
   // ---- batch-mean loss

@@ -178,7 +178,7 @@ def run_ours(args, rank, world, local_rank):
 
     import synth
     from paper_2407_09543_b200 import ntbc
-    from paper_2407_09543_b200.shard import PeerGather, gather_materials
+    from paper_2407_09543_b200.shard import PeerGather, PeerRows, gather_materials
 
     # NTBC_BENCH_ONE_GPU=1: functional check of the multi-rank path on a one-GPU box (every rank on cuda:0,
     # gloo process group; the ranks' kernels never wait on each other).  Its numbers are not measurements.
@@ -238,6 +238,39 @@ def run_ours(args, rank, world, local_rank):
         assert torch.equal(pg.buf[0], out_all), "peer gather: rank 0 slice differs from a local decode"
     times = [a.elapsed_time(b) for a, b in evs]
     t_ms = sum(times) / len(times)
+
+    # ---- latency view (N > 1, peer gather): ONE material split by block rows over the ranks, every rank
+    # decoding its rows straight into rank 0's buffer; time = max over ranks (the metric's "ms per 4k
+    # material at N GPUs" as a single-material latency, beside the weak-scaling throughput above)
+    lat_ms = None
+    if pg is not None:
+        pr = PeerRows(n_tex, BH, BW, rank, world, dev)
+        if pr.ok:
+            model0 = ntbc.Model(synth.model_blob(args.config, material=0), local_rank)   # one material on all ranks
+
+            def lat_step():
+                ntbc.decode_material([model0], W, H, row_begin=pr.r0, row_end=pr.r1, out_ptrs=pr.ptrs, stream=stream)
+                pr.complete()
+            for _ in range(3):
+                lat_step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            for s_ in range(args.steps):
+                flush.zero_()
+                lev[s_][0].record(stream)
+                lat_step()
+                lev[s_][1].record(stream)
+            torch.cuda.synchronize()
+            lt = torch.tensor([sum(a.elapsed_time(b) for a, b in lev) / args.steps], device=dev, dtype=torch.float64)
+            dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+            lat_ms = float(lt.item())
+            if rank == 0:   # rank 0's buffer holds the whole material: it must equal a local decode
+                ref = torch.stack(ntbc.decode_material([model0], W, H, stream=stream))
+                torch.cuda.synchronize()
+                assert torch.equal(pr.buf, ref), "row-split peer decode differs from a local decode"
+        pr.close()
+        dist.barrier()
     t_tensor = torch.tensor([t_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
@@ -318,7 +351,8 @@ def run_ours(args, rank, world, local_rank):
                               "buffer over NVLink (CUDA IPC), completion by a 1-element all-reduce",
                               "nccl": "separate NCCL gather after the decode"}[gather_mode],
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "ms_per_4k_material": t_ms_max / world if world > 1 else t_ms_max},
+                   "ms_per_4k_material": t_ms_max / world if world > 1 else t_ms_max,
+                   "latency_ms_per_4k_material": lat_ms if world > 1 else t_ms_max},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
                      "frac": achieved / alu_peak, "traffic": traffic,
                      "kernel": "fused_decode_kernel", "kernel_ms": k_ms,

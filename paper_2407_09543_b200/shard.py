@@ -62,44 +62,36 @@ def gather_materials(local: torch.Tensor, rank: int, world: int, group=None):
     return bufs if rank == 0 else None
 
 
-class PeerGather:
-    """Fused gather of one [n_tex, BH, BW] material per rank into rank 0's [world, n_tex, BH, BW] buffer.
+class _PeerBuffer:
+    """Rank 0 allocates an int64 device buffer of `shape` and exports it (ntbc_peer_export); the handle is
+    broadcast with the process group; every other rank maps it (ntbc_peer_open).  `base` is the buffer's
+    address in this rank's address space.  The ranks agree on success (an all-reduce of the outcome), so
+    they fall back together when IPC or peer access is unavailable."""
 
-    Rank 0 allocates the buffer and exports it (ntbc_peer_export); the handle is broadcast with the
-    process group; every other rank maps it (ntbc_peer_open) and decodes straight into its slice
-    (ntbc.decode_material(..., out_ptrs=self.ptrs)).  `complete()` is the only exchange on the timed
-    path: a one-element all-reduce ordered after the decode on every rank, after which rank 0's
-    buffer holds all materials (the writes are system-scope fenced by the fused kernel)."""
-
-    def __init__(self, n_tex: int, bh: int, bw: int, rank: int, world: int, device: torch.device, group=None):
+    def __init__(self, shape, rank: int, world: int, device: torch.device, group=None):
         from . import ntbc   # CUDA only; the CPU helpers above do not need the library
         self.rank, self.world, self.group, self._opened = rank, world, group, None
-        self.buf, self.ptrs, self.error = None, None, None
+        self.buf, self.base, self.error = None, None, None
         handle = None
         if rank == 0:
             try:
-                self.buf = torch.empty((world, n_tex, bh, bw), dtype=torch.int64, device=device)
+                self.buf = torch.empty(shape, dtype=torch.int64, device=device)
                 handle = ntbc.peer_export(self.buf)
             except Exception as e:   # e.g. an allocator without IPC support
                 self.error = f"export: {e}"
         obj = [handle]
         dist.broadcast_object_list(obj, src=0, group=group)
-        base = None
         if rank == 0:
-            base = self.buf.data_ptr() if handle is not None else None
+            self.base = self.buf.data_ptr() if handle is not None else None
         elif obj[0] is not None:
             try:
-                base = self._opened = ntbc.peer_open(obj[0], device.index)
+                self.base = self._opened = ntbc.peer_open(obj[0], device.index)
             except Exception as e:   # no peer access between these GPUs
                 self.error = f"open: {e}"
-        # every rank must agree, or the ranks would run different exchanges
-        ok = torch.tensor([1 if base is not None else 0], dtype=torch.int32,
+        ok = torch.tensor([1 if self.base is not None else 0], dtype=torch.int32,
                           device=device if dist.get_backend(group) == "nccl" else "cpu")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
         self.ok = bool(ok.item())
-        if self.ok:
-            plane = bh * bw * 8
-            self.ptrs = [base + (rank * n_tex + k) * plane for k in range(n_tex)]
         self._flag = torch.zeros(1, dtype=torch.int32, device=device)
 
     def complete(self):
@@ -118,3 +110,28 @@ class PeerGather:
             torch.cuda.synchronize()
             ntbc.peer_close(self._opened)
             self._opened = None
+
+
+class PeerGather(_PeerBuffer):
+    """Fused gather of one [n_tex, BH, BW] material per rank into rank 0's [world, n_tex, BH, BW] buffer
+    (throughput view: weak scaling over materials).  Every rank decodes straight into its slice
+    (ntbc.decode_material(..., out_ptrs=self.ptrs)); `complete()` is the only exchange on the timed path,
+    after which rank 0's buffer holds all materials (the writes are system-scope fenced by the fused
+    kernel)."""
+
+    def __init__(self, n_tex: int, bh: int, bw: int, rank: int, world: int, device: torch.device, group=None):
+        super().__init__((world, n_tex, bh, bw), rank, world, device, group)
+        plane = bh * bw * 8
+        self.ptrs = [self.base + (rank * n_tex + k) * plane for k in range(n_tex)] if self.ok else None
+
+
+class PeerRows(_PeerBuffer):
+    """One material split by block rows over the ranks (latency view): rank r decodes the rows
+    row_shards(BH, world)[r] straight into those rows of rank 0's [n_tex, BH, BW] buffer
+    (ntbc.decode_material(..., row_begin=self.r0, row_end=self.r1, out_ptrs=self.ptrs))."""
+
+    def __init__(self, n_tex: int, bh: int, bw: int, rank: int, world: int, device: torch.device, group=None):
+        super().__init__((n_tex, bh, bw), rank, world, device, group)
+        self.r0, self.r1 = row_shards(bh, world)[rank]
+        plane = bh * bw * 8
+        self.ptrs = [self.base + k * plane + self.r0 * bw * 8 for k in range(n_tex)] if self.ok else None

@@ -945,10 +945,16 @@ ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const 
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static bool pack_configured = false;
+  if (!pack_configured) {
+    CUDA_TRY(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    pack_configured = true;
+  }
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_kernel, 256, smem));
   // persistent grid: exactly the resident CTAs (a second partial wave of grid-stride CTAs would double
   // the tail), each striding over 16-block tiles
   const int grid = std::max(1, std::min(p.n_tiles, sms * std::max(per_sm, 1)));
+  if (smem > 227 * 1024) return fail(NTBC_EINVAL, "pack tile needs %zu B of shared memory", smem);
   pack_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(p);
   g_launches++;
   CUDA_TRY(cudaGetLastError());

@@ -426,9 +426,9 @@ struct PackParams {
   int fmt[kMaxTex], ep_off[kMaxTex], col_off[kMaxTex];
   uint64_t* out[kMaxTex];
 };
-constexpr int kPackTileBlocks = 16;   // block positions per tile (one block row): 64 texel columns x 4 rows
+constexpr int kPackTileBlocks = 64;   // block positions per tile (one block row): 256 texel columns x 4 rows
 
-// Per tile: the tile's fp32 MLP outputs (4 texel rows x 64 texels x N_c, and 16 x N_e) are staged in
+// Per tile: the tile's fp32 MLP outputs (4 texel rows x 256 texels x N_c, and 64 x N_e) are staged in
 // shared memory with coalesced 16-B loads (the only HBM traffic besides the BC words: every input byte
 // is read once); one thread per (block, texture) quantizes the endpoints into the BC word header (R11-R13);
 // then one warp per two blocks, lane = texel, rebuilds each palette from its header and the exact UNORM
@@ -447,9 +447,9 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
   extern __shared__ __align__(16) float psm[];
   float* s_unorm = psm;                                   // 352 UNORM quotients + 32 BC4 weights
   const int rs = 4 * kPackTileBlocks * p.n_c + 4;         // texel-row stride (+4 floats: rows start 4 banks apart)
-  float* s_col = psm + 384;                               // [4][64 * N_c + 4]
-  float* s_ep = s_col + 4 * rs;                           // [16][N_e]
-  uint32_t* s_hdr = reinterpret_cast<uint32_t*>(s_ep + kPackTileBlocks * p.n_e);   // [16][n_tex]
+  float* s_col = psm + 384;                               // [4][256 * N_c + 4]
+  float* s_ep = s_col + 4 * rs;                           // [64][N_e]
+  uint32_t* s_hdr = reinterpret_cast<uint32_t*>(s_ep + kPackTileBlocks * p.n_e);   // [64][kMaxTex]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 352; i += blockDim.x)
     s_unorm[i] = i < 32 ? __fdiv_rn((float)i, 31.0f) : i < 96 ? __fdiv_rn((float)(i - 32), 63.0f)
@@ -464,8 +464,8 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
                  4 * nb * p.n_c);
     pack_stage(s_ep, p.ep + ((size_t)row * p.BW + bx0) * p.n_e, nb * p.n_e);
     __syncthreads();
-    if (tid < nb * p.n_tex) {   // BC word headers: quantized endpoints (R11-R13)
-      const int b = tid / p.n_tex, k = tid - b * p.n_tex;
+    for (int bk = tid; bk < nb * p.n_tex; bk += blockDim.x) {   // BC word headers: quantized endpoints (R11-R13)
+      const int b = bk / p.n_tex, k = bk - b * p.n_tex;
       const float* e = s_ep + b * p.n_e + p.ep_off[k];
       if (p.fmt[k] == kFmtBC1) {
         float ep6[6];

@@ -55,6 +55,9 @@ struct FusedParams {
   int tail_row0, tail_rows;     // ... and per (smaller) chunk from tail_row0 on (local rows)
   int* next_unit;               // optional: dynamic unit counter (zeroed before the launch)
   int naive;                    // 1: the texel net outputs one weight per texture (naive approach)
+  int pal_off[kMaxTex];         // per texture: float offset of its palette in a block's palette record
+  int pal_stride;               // floats per block palette record (BC1 12, BC4 8 per texture)
+  uint32_t tpal_off;            // byte offset of the colour tile's palettes inside a work group's region
 };
 
 // ---------------------------------------------------------------- a2 at model upload: Eq.2 dequantization
@@ -166,6 +169,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   float* stage = reinterpret_cast<float*>(A);                     // [ch][128] fp32 (after the last MMA)
   uint32_t* hdrs = reinterpret_cast<uint32_t*>(wg_base + p.a_bytes);  // [tex][128 blocks] BC word low bits
   uint8_t* swp = reinterpret_cast<uint8_t*>(hdrs + p.n_tex * 128);   // [tex][128 blocks] BC1 endpoint swap (naive)
+  float* tpal = reinterpret_cast<float*>(wg_base + p.a_bytes + p.tpal_off);   // [8 blocks][pal_stride] colour tile palettes
   uint64_t* bars = reinterpret_cast<uint64_t*>(ones + 4096 + kUnormBytes + NWG * (p.a_bytes + p.pal_bytes));
   uint64_t* bar_mma = bars + wg;                                  // this work group's MMA completion
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
@@ -348,6 +352,20 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       const int b = 8 * j + (r >> 4), i = r & 15;
       const int bx = bx0 + b, x = 4 * min(bx, p.BW - 1) + (i & 3), y = 4 * by + (i >> 2);
       named_bar_sync(bar_id, 128);
+      if (!DUMP && !NAIVE && r < 8 * p.n_tex) {   // the tile's 8 x n_tex palettes, once per block (Eq.7/8, R18)
+        const int bl = r / p.n_tex, k = r - bl * p.n_tex;
+        const uint32_t hdr = hdrs[k * 128 + 8 * j + bl];
+        float* dst = tpal + bl * p.pal_stride + p.pal_off[k];
+        if (p.fmt[k] == kFmtBC1) {
+          const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
+          const float e0[3] = {unorm[c0 >> 11], unorm[32 + ((c0 >> 5) & 63)], unorm[c0 & 31]};
+          const float e1[3] = {unorm[c1 >> 11], unorm[32 + ((c1 >> 5) & 63)], unorm[c1 & 31]};
+          bc1_palette_pairs(e0, e1, dst);
+        } else {
+          const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
+          bc4_palette_tab(unorm[96 + E0], unorm[96 + E1], E0 > E1, unorm + 352, dst);
+        }
+      }
       {
         const float pu = __fdiv_rn(__fadd_rn((float)x, 0.5f), (float)p.W);
         const float pv = __fdiv_rn(__fadd_rn((float)y, 0.5f), (float)p.H);
@@ -380,18 +398,16 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
               const uint32_t map = E0 > E1 ? 0x17654320u : 0x71543206u;
               word = (uint64_t)hdr | (pack_bc4_indices((map >> (4 * n)) & 7u, lane) << 16);
             }
-          } else if (p.fmt[k] == kFmtBC1) {  // palette endpoints = UNORM expansion of the header (R12)
-            const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
-            const float e0[3] = {unorm[c0 >> 11], unorm[32 + ((c0 >> 5) & 63)], unorm[c0 & 31]};
-            const float e1[3] = {unorm[c1 >> 11], unorm[32 + ((c1 >> 5) & 63)], unorm[c1 & 31]};
+          } else if (p.fmt[k] == kFmtBC1) {  // the block's palette (precomputed at the tile start)
+            const float2* P = reinterpret_cast<const float2*>(tpal + (r >> 4) * p.pal_stride + p.pal_off[k]);
             const float c[3] = {stage[co * 128 + r], stage[(co + 1) * 128 + r], stage[(co + 2) * 128 + r]};
-            const uint32_t code = bc1_code(c, e0, e1, c0 == c1);
+            const uint32_t code = bc1_code_pairs(c, P, (hdr & 0xFFFFu) == (hdr >> 16));
             word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
           } else {
-            const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
-            float pl[8];
-            bc4_palette_tab(unorm[96 + E0], unorm[96 + E1], E0 > E1, unorm + 352, pl);
-            const uint32_t code = bc4_code(stage[co * 128 + r], pl, E0 > E1);
+            const float4* P = reinterpret_cast<const float4*>(tpal + (r >> 4) * p.pal_stride + p.pal_off[k]);
+            const float4 q0 = P[0], q1 = P[1];
+            const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            const uint32_t code = bc4_code(stage[co * 128 + r], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu));
             word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
           }
           if ((lane & 15) == 0 && b < nvalid) p.out[k][out_row + bx] = word;

@@ -173,23 +173,27 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
   for (int l = 0; l < 3; l++) {
     const float* a = A[l] + tid * ldA[l];
     float* o = A[l + 1] + tid * LD;
-    float z[HQ];
+    uint64_t z2[HQ / 2];   // output pairs, packed FFMA2 (each lane the same RN fma as the scalar form)
 #pragma unroll
-    for (int jj = 0; jj < HQ; jj++) z[jj] = sb[l][h * HQ + jj];
+    for (int jj = 0; jj < HQ / 2; jj++) z2[jj] = f2pack(sb[l][h * HQ + 2 * jj], sb[l][h * HQ + 2 * jj + 1]);
     for (int k = 0; k < p.kin[l]; k++) {
       const float ak = a[k];
+      const uint64_t a2 = f2pack(ak, ak);
       const float4* w4 = reinterpret_cast<const float4*>(sW[l] + k * HID + h * HQ);
 #pragma unroll
       for (int q4 = 0; q4 < HQ / 4; q4++) {
         const float4 w = w4[q4];
-        z[4 * q4] = __fmaf_rn(ak, w.x, z[4 * q4]);
-        z[4 * q4 + 1] = __fmaf_rn(ak, w.y, z[4 * q4 + 1]);
-        z[4 * q4 + 2] = __fmaf_rn(ak, w.z, z[4 * q4 + 2]);
-        z[4 * q4 + 3] = __fmaf_rn(ak, w.w, z[4 * q4 + 3]);
+        z2[2 * q4] = fma2(a2, f2pack(w.x, w.y), z2[2 * q4]);
+        z2[2 * q4 + 1] = fma2(a2, f2pack(w.z, w.w), z2[2 * q4 + 1]);
       }
     }
 #pragma unroll
-    for (int jj = 0; jj < HQ; jj++) o[h * HQ + jj] = selu_f(z[jj]);
+    for (int jj = 0; jj < HQ / 2; jj++) {
+      float z0, z1;
+      f2unpack(z2[jj], z0, z1);
+      o[h * HQ + 2 * jj] = selu_f(z0);
+      o[h * HQ + 2 * jj + 1] = selu_f(z1);
+    }
     __syncthreads();
   }
   float* D = Dl;
@@ -332,19 +336,22 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
       const int nblk = (K / 2) * (N / 4);
       for (int e = t; e < nblk; e += NT) {
         const int kp = e / (N / 4), jq = e - kp * (N / 4), k = 2 * kp, j = 4 * jq;
-        float acc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
+        uint64_t acc[2][2] = {{0ull, 0ull}, {0ull, 0ull}};   // (j, j+1), (j+2, j+3) pairs, packed FFMA2
         for (int i = 0; i < kTrainTile; i++) {
-          const float a0 = A[l][i * ldA[l] + k], a1 = A[l][i * ldA[l] + k + 1];
+          const float as0 = A[l][i * ldA[l] + k], as1 = A[l][i * ldA[l] + k + 1];   // ldA[0] is odd
           const float4 d = *reinterpret_cast<const float4*>(D + i * LD + j);
-          acc[0][0] = __fmaf_rn(a0, d.x, acc[0][0]); acc[0][1] = __fmaf_rn(a0, d.y, acc[0][1]);
-          acc[0][2] = __fmaf_rn(a0, d.z, acc[0][2]); acc[0][3] = __fmaf_rn(a0, d.w, acc[0][3]);
-          acc[1][0] = __fmaf_rn(a1, d.x, acc[1][0]); acc[1][1] = __fmaf_rn(a1, d.y, acc[1][1]);
-          acc[1][2] = __fmaf_rn(a1, d.z, acc[1][2]); acc[1][3] = __fmaf_rn(a1, d.w, acc[1][3]);
+          const uint64_t dxy = f2pack(d.x, d.y), dzw = f2pack(d.z, d.w);
+          const uint64_t a0 = f2pack(as0, as0), a1 = f2pack(as1, as1);
+          acc[0][0] = fma2(a0, dxy, acc[0][0]); acc[0][1] = fma2(a0, dzw, acc[0][1]);
+          acc[1][0] = fma2(a1, dxy, acc[1][0]); acc[1][1] = fma2(a1, dzw, acc[1][1]);
         }
 #pragma unroll
-        for (int r = 0; r < 2; r++)   // one 16-byte vector atomic per 4 consecutive weights (sm_90+)
-          atomicAdd(reinterpret_cast<float4*>(p.grads + p.w_off[l] + (size_t)(k + r) * N + j),
-                    make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
+        for (int r = 0; r < 2; r++) {   // one 16-byte vector atomic per 4 consecutive weights (sm_90+)
+          float4 g4;
+          f2unpack(acc[r][0], g4.x, g4.y);
+          f2unpack(acc[r][1], g4.z, g4.w);
+          atomicAdd(reinterpret_cast<float4*>(p.grads + p.w_off[l] + (size_t)(k + r) * N + j), g4);
+        }
       }
     } else {
       for (int e = t; e < K * N; e += NT) {
@@ -367,15 +374,23 @@ __global__ void __launch_bounds__(kTrainTile * kTrainQ, 1) train_step_kernel(con
     for (int kk = 0; kk < HID / kTrainQ; kk++) dA[kk] = 0.0f;
     if (N % 4 == 0) {   // per j quad: one float4 of this sample's delta row, one float4 per W row (broadcast)
       const float4* d4 = reinterpret_cast<const float4*>(D + tid * LD);
+      uint64_t dA2[HID / kTrainQ / 2];   // input pairs (kk, kk+1), packed FFMA2, same per-lane fma chain
+#pragma unroll
+      for (int kp = 0; kp < HID / kTrainQ / 2; kp++) dA2[kp] = 0ull;
       for (int jq = 0; jq < N / 4; jq++) {
         const float4 d = d4[jq];
+        const uint64_t dx = f2pack(d.x, d.x), dy = f2pack(d.y, d.y), dz = f2pack(d.z, d.z), dw = f2pack(d.w, d.w);
 #pragma unroll
-        for (int kk = 0; kk < HID / kTrainQ; kk++) {
-          if (k0 + kk >= k1) break;
-          const float4 w = *reinterpret_cast<const float4*>(sW[l] + (k0 + kk) * N + 4 * jq);
-          dA[kk] = __fmaf_rn(w.w, d.w, __fmaf_rn(w.z, d.z, __fmaf_rn(w.y, d.y, __fmaf_rn(w.x, d.x, dA[kk]))));
+        for (int kp = 0; kp < HID / kTrainQ / 2; kp++) {
+          if (k0 + 2 * kp >= k1) break;
+          const float4 wa = *reinterpret_cast<const float4*>(sW[l] + (k0 + 2 * kp) * N + 4 * jq);
+          const float4 wb = *reinterpret_cast<const float4*>(sW[l] + min(k0 + 2 * kp + 1, k1 - 1) * N + 4 * jq);
+          dA2[kp] = fma2(f2pack(wa.w, wb.w), dw, fma2(f2pack(wa.z, wb.z), dz,
+                    fma2(f2pack(wa.y, wb.y), dy, fma2(f2pack(wa.x, wb.x), dx, dA2[kp]))));
         }
       }
+#pragma unroll
+      for (int kp = 0; kp < HID / kTrainQ / 2; kp++) f2unpack(dA2[kp], dA[2 * kp], dA[2 * kp + 1]);
     } else {
       for (int k = k0; k < k1; k++)
         for (int j = 0; j < N; j++) dA[k - k0] = __fmaf_rn(sW[l][k * N + j], D[tid * LD + j], dA[k - k0]);

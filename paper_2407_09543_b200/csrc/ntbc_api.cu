@@ -266,7 +266,7 @@ ntbc_status launch_fused_t(const FusedParams& p, size_t smem, int grid, cudaStre
 }
 
 size_t fused_smem(const FusedParams& p, int nwg) {
-  return (size_t)p.net[0].img_bytes + p.net[1].img_bytes + 4096 + kUnormBytes +
+  return (size_t)p.net[0].img_bytes + p.net[1].img_bytes + kOnesBytes + kUnormBytes +
          (size_t)nwg * (p.a_bytes + p.pal_bytes) + 8 * nwg + 16 + 4 * 8;
 }
 
@@ -317,7 +317,7 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
   const int maxo = a.dims[0][4] > a.dims[1][4] ? a.dims[0][4] : a.dims[1][4];
   const uint32_t a_kmajor = 128u * a.hidden * 2u, a_stage = 128u * 4u * (uint32_t)((maxo + 1) & ~1);  // pairs
   p.a_bytes = (uint32_t)((std::max(a_kmajor, a_stage) + 127) & ~127u);
-  // per work group: BC word headers + BC1 swap flags of the unit's 128 blocks, then the palettes of the
+  // per work group: BC word headers (+ BC1 swap flags, naive models) of the unit's 128 blocks, then the palettes of the
   // current colour tile's 8 blocks (BC1 12 floats, BC4 8 floats per texture; 16-B aligned records)
   p.pal_stride = 0;
   for (int k = 0; k < a.n_tex; k++) {
@@ -325,7 +325,7 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
     p.pal_stride += a.fmt[k] == NTBC_BC1 ? 12 : 8;
   }
   p.pal_stride = (p.pal_stride + 3) & ~3;
-  p.tpal_off = (uint32_t)((a.n_tex * 128 * 5 + 15) & ~15u);
+  p.tpal_off = (uint32_t)((a.n_tex * 128 * (a.naive ? 5 : 4) + 15) & ~15u);   // BC1 swap flags: naive only
   p.pal_bytes = p.tpal_off + (uint32_t)(8 * p.pal_stride * sizeof(float));
   p.naive = a.naive;
   int dev = 0, sms = 148;

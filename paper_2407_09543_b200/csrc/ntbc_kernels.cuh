@@ -19,6 +19,7 @@ constexpr int kMaxLevels = 8;
 constexpr int kUnitBlocks = 128;  // block positions per work unit = rows of one endpoint MMA tile
 constexpr int kFmtBC1 = 1;
 
+constexpr int kOnesBytes = 256;    // the bias MMA's ones tile: one 8-row group, read with SBO = 0
 constexpr int kUnormBytes = 1536;  // 352 fp32 UNORM expansion values (q/31, q/63, q/255) + 32 BC4 weights
 
 struct GridLevel {
@@ -141,7 +142,7 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, in
                                             uint32_t b_base, int kin16, int N) {
   const int K_B = kin16 + 16;
   const uint32_t idesc = idesc_f16_f32(128, N);
-  mma_f16(tmem_d, smem_desc(ones_base, 128, 256), smem_desc(b_base + (kin16 / 16) * 256, 128, K_B * 16), idesc, 0u);
+  mma_f16(tmem_d, smem_desc(ones_base, 128, 0), smem_desc(b_base + (kin16 / 16) * 256, 128, K_B * 16), idesc, 0u);
   for (int c = 0; c < kin16 / 16; c++)
     mma_f16(tmem_d, smem_desc(a_base + c * 256, 128, K_A * 16), smem_desc(b_base + c * 256, 128, K_B * 16), idesc,
             1u);
@@ -162,15 +163,15 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   // ---- carve shared memory
   uint8_t* img_e = smem;                                          // endpoint net operand image
   uint8_t* img_c = smem + p.net[0].img_bytes;                     // colour net operand image
-  uint8_t* ones = img_c + p.net[1].img_bytes;                     // [128][16] K-major, column 0 = 1.0
-  float* unorm = reinterpret_cast<float*>(ones + 4096);           // q/31 [32], q/63 [64], q/255 [256], BC4 weights
-  uint8_t* wg_base = ones + 4096 + kUnormBytes + wg * (p.a_bytes + p.pal_bytes);
+  uint8_t* ones = img_c + p.net[1].img_bytes;                     // [8][16] K-major, column 0 = 1.0
+  float* unorm = reinterpret_cast<float*>(ones + kOnesBytes);           // q/31 [32], q/63 [64], q/255 [256], BC4 weights
+  uint8_t* wg_base = ones + kOnesBytes + kUnormBytes + wg * (p.a_bytes + p.pal_bytes);
   uint8_t* A = wg_base;                                           // [128][H] K-major fp16 / fp32 staging
   float* stage = reinterpret_cast<float*>(A);                     // [ch][128] fp32 (after the last MMA)
   uint32_t* hdrs = reinterpret_cast<uint32_t*>(wg_base + p.a_bytes);  // [tex][128 blocks] BC word low bits
   uint8_t* swp = reinterpret_cast<uint8_t*>(hdrs + p.n_tex * 128);   // [tex][128 blocks] BC1 endpoint swap (naive)
   float* tpal = reinterpret_cast<float*>(wg_base + p.a_bytes + p.tpal_off);   // [8 blocks][pal_stride] colour tile palettes
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ones + 4096 + kUnormBytes + NWG * (p.a_bytes + p.pal_bytes));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ones + kOnesBytes + kUnormBytes + NWG * (p.a_bytes + p.pal_bytes));
   uint64_t* bar_mma = bars + wg;                                  // this work group's MMA completion
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
   int* next_slot = reinterpret_cast<int*>(tmem_slot + 1) + wg;    // dynamic scheduling: this group's next unit
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       }
     }
   }
-  if (tid < 128) {  // the constant ones tile used to fold the bias into the MMA
+  if (tid < 8) {  // the constant ones tile used to fold the bias into the MMA (all 16 row groups read it)
     const uint4 c0 = make_uint4(0x3C00u, 0u, 0u, 0u), z = make_uint4(0u, 0u, 0u, 0u);
     *reinterpret_cast<uint4*>(ones + kmajor_offset(tid, 0, 16)) = c0;
     *reinterpret_cast<uint4*>(ones + kmajor_offset(tid, 8, 16)) = z;

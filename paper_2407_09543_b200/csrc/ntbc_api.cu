@@ -942,28 +942,36 @@ ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const 
     if (fmts[k] != NTBC_BC1 && fmts[k] != NTBC_BC4) return fail(NTBC_EINVAL, "bad format %d", fmts[k]);
     if (!out_blocks[k] || ((uintptr_t)out_blocks[k] & 7)) return fail(NTBC_EINVAL, "out_blocks[%d] NULL or misaligned", k);
     p.fmt[k] = fmts[k]; p.ep_off[k] = eo; p.col_off[k] = co; p.out[k] = (uint64_t*)out_blocks[k];
+    p.pal_off[k] = p.pal_stride;
     eo += fmts[k] == NTBC_BC1 ? 6 : 2;
     co += fmts[k] == NTBC_BC1 ? 3 : 1;
+    p.pal_stride += fmts[k] == NTBC_BC1 ? 12 : 8;
   }
   p.n_e = eo; p.n_c = co;
   p.tiles_per_row = (p.BW + kPackTileBlocks - 1) / kPackTileBlocks;
   p.n_tiles = p.tiles_per_row * p.rows;
-  const size_t smem = (384 + 4 * (4 * kPackTileBlocks * p.n_c + 4) + kPackTileBlocks * p.n_e) * sizeof(float) +
+  const size_t smem = (384 + (size_t)kPackStages * (4 * (4 * kPackTileBlocks * p.n_c + 4) +
+                                                    ((kPackTileBlocks * p.n_e + 3) & ~3)) +
+                       (NTBC_PACK_PAL ? (size_t)kPackTileBlocks * p.pal_stride : 0)) * sizeof(float) +
                       kPackTileBlocks * kMaxTex * sizeof(uint32_t);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  static bool pack_configured = false;
-  if (!pack_configured) {
-    CUDA_TRY(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    pack_configured = true;
+  static void (*const kernels[kMaxTex])(PackParams) = {pack_kernel<1>, pack_kernel<2>, pack_kernel<3>, pack_kernel<4>,
+                                                       pack_kernel<5>, pack_kernel<6>, pack_kernel<7>, pack_kernel<8>};
+  static_assert(kMaxTex == 8, "pack kernel instantiations");
+  const auto kern = kernels[n_tex - 1];
+  static bool pack_configured[kMaxTex] = {};
+  if (!pack_configured[n_tex - 1]) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    pack_configured[n_tex - 1] = true;
   }
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_kernel, 256, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPackThreads, smem));
   // persistent grid: exactly the resident CTAs (a second partial wave of grid-stride CTAs would double
   // the tail), each striding over 16-block tiles
   const int grid = std::max(1, std::min(p.n_tiles, sms * std::max(per_sm, 1)));
   if (smem > 227 * 1024) return fail(NTBC_EINVAL, "pack tile needs %zu B of shared memory", smem);
-  pack_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(p);
+  kern<<<grid, kPackThreads, smem, (cudaStream_t)stream>>>(p);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return NTBC_OK;

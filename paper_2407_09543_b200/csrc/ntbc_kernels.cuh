@@ -441,58 +441,112 @@ struct PackParams {
   const float* col;  // [rows*4][W][N_c]
   int W, BW, rows, n_e, n_c, n_tex, tiles_per_row, n_tiles;
   int fmt[kMaxTex], ep_off[kMaxTex], col_off[kMaxTex];
+  int pal_off[kMaxTex], pal_stride;   // per block: BC1 12 / BC4 8 palette floats per texture
   uint64_t* out[kMaxTex];
 };
 constexpr int kPackTileBlocks = 64;   // block positions per tile (one block row): 256 texel columns x 4 rows
 
+#ifndef NTBC_PACK_STAGES
+#define NTBC_PACK_STAGES 1      // tile buffers in shared memory: 2 = the next tile's loads overlap this tile's math
+#endif
+#ifndef NTBC_PACK_PAL
+#define NTBC_PACK_PAL 0         // 1 = palettes built once per block in shared memory (measured slower)
+#endif
+#ifndef NTBC_PACK_THREADS
+#define NTBC_PACK_THREADS 256
+#endif
+constexpr int kPackStages = NTBC_PACK_STAGES, kPackThreads = NTBC_PACK_THREADS;
+
 // Per tile: the tile's fp32 MLP outputs (4 texel rows x 256 texels x N_c, and 64 x N_e) are staged in
-// shared memory with coalesced 16-B loads (the only HBM traffic besides the BC words: every input byte
-// is read once); one thread per (block, texture) quantizes the endpoints into the BC word header (R11-R13);
-// then one warp per two blocks, lane = texel, rebuilds each palette from its header and the exact UNORM
-// tables, selects indices and packs the words as in the fused kernel's epilogue.
+// shared memory with asynchronous copies (cp.async, 16 B where the source is 16-B aligned, else 8 or 4 B;
+// every input byte is read once, the only HBM traffic besides the BC words), issued one tile ahead into
+// the other of kPackStages buffers when kPackStages = 2 (measured slower than one buffer with more CTAs
+// per SM: the kernel is issue-bound); one thread per (block, texture) quantizes the
+// endpoints into the BC word header (R11-R13) and builds the block's palette from it and the exact UNORM
+// tables (Eq.7/8, R18) in shared memory; then one warp per two blocks, lane = texel, selects indices
+// and packs the words with the fused kernel's epilogue functions.
 __device__ __forceinline__ void pack_stage(float* dst, const float* src, int n) {
+  const uint32_t d = smem_u32(dst);
   if ((((uintptr_t)src) & 15) == 0 && (n & 3) == 0) {
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    for (int i = threadIdx.x; i < n / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+    for (int i = threadIdx.x; i < n / 4; i += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * i), "l"(src + 4 * i) : "memory");
+  } else if ((((uintptr_t)src) & 7) == 0 && (n & 1) == 0) {
+    for (int i = threadIdx.x; i < n / 2; i += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d + 8 * i), "l"(src + 2 * i) : "memory");
   } else {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d + 4 * i), "l"(src + i) : "memory");
   }
 }
 
-__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams p) {
+__device__ __forceinline__ void pack_issue(const PackParams& p, int t, float* s_col, float* s_ep, int rs) {
+  if (t < p.n_tiles) {
+    const int row = t / p.tiles_per_row, bx0 = (t - row * p.tiles_per_row) * kPackTileBlocks;
+    const int nb = min(kPackTileBlocks, p.BW - bx0);
+    for (int yi = 0; yi < 4; yi++)
+      pack_stage(s_col + yi * rs, p.col + ((size_t)(4 * row + yi) * p.W + 4 * bx0) * p.n_c, 4 * nb * p.n_c);
+    pack_stage(s_ep, p.ep + ((size_t)row * p.BW + bx0) * p.n_e, nb * p.n_e);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");   // one group per tile (empty past the end)
+}
+
+// NT = the texture count as a template parameter (1..kMaxTex): the texture loop unrolls, so each texture's
+// format, offsets and output pointer are immediates of the parameter bank instead of indexed loads
+template <int NT>
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constant__ PackParams p) {
   extern __shared__ __align__(16) float psm[];
   float* s_unorm = psm;                                   // 352 UNORM quotients + 32 BC4 weights
   const int rs = 4 * kPackTileBlocks * p.n_c + 4;         // texel-row stride (+4 floats: rows start 4 banks apart)
-  float* s_col = psm + 384;                               // [4][256 * N_c + 4]
-  float* s_ep = s_col + 4 * rs;                           // [64][N_e]
-  uint32_t* s_hdr = reinterpret_cast<uint32_t*>(s_ep + kPackTileBlocks * p.n_e);   // [64][kMaxTex]
+  const int stage_floats = 4 * rs + ((kPackTileBlocks * p.n_e + 3) & ~3);
+  float* s_pal = psm + 384 + kPackStages * stage_floats;                                   // [64][pal_stride]
+  uint32_t* s_hdr = reinterpret_cast<uint32_t*>(s_pal + (NTBC_PACK_PAL ? kPackTileBlocks * p.pal_stride : 0));   // [64][kMaxTex]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 352; i += blockDim.x)
     s_unorm[i] = i < 32 ? __fdiv_rn((float)i, 31.0f) : i < 96 ? __fdiv_rn((float)(i - 32), 63.0f)
                                                             : __fdiv_rn((float)(i - 96), 255.0f);
   if (tid < 32) s_unorm[352 + tid] = bc4_weight(tid);
-  for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+  int it = 0;
+  if (kPackStages > 1) pack_issue(p, blockIdx.x, psm + 384, psm + 384 + 4 * rs, rs);
+  for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, it++) {
     const int row = t / p.tiles_per_row, bx0 = (t - row * p.tiles_per_row) * kPackTileBlocks;
     const int nb = min(kPackTileBlocks, p.BW - bx0);
+    float* s_col = psm + 384 + (it % kPackStages) * stage_floats;   // [4][256 * N_c + 4]
+    float* s_ep = s_col + 4 * rs;                                    // [64][N_e]
     __syncthreads();   // previous tile's readers are done (and the tables are written)
-    for (int yi = 0; yi < 4; yi++)
-      pack_stage(s_col + yi * rs, p.col + ((size_t)(4 * row + yi) * p.W + 4 * bx0) * p.n_c,
-                 4 * nb * p.n_c);
-    pack_stage(s_ep, p.ep + ((size_t)row * p.BW + bx0) * p.n_e, nb * p.n_e);
+    if (kPackStages > 1) {
+      float* n_col = psm + 384 + ((it + 1) % kPackStages) * stage_floats;
+      pack_issue(p, t + gridDim.x, n_col, n_col + 4 * rs, rs);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");   // this tile's copies (issued one tile ago) landed
+    } else {
+      pack_issue(p, t, s_col, s_ep, rs);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
-    for (int bk = tid; bk < nb * p.n_tex; bk += blockDim.x) {   // BC word headers: quantized endpoints (R11-R13)
+    for (int bk = tid; bk < nb * p.n_tex; bk += blockDim.x) {   // BC word headers (R11-R13) and palettes
       const int b = bk / p.n_tex, k = bk - b * p.n_tex;
       const float* e = s_ep + b * p.n_e + p.ep_off[k];
+      float* dst = s_pal + b * p.pal_stride + p.pal_off[k];
       if (p.fmt[k] == kFmtBC1) {
         float ep6[6];
 #pragma unroll
         for (int c = 0; c < 6; c++) ep6[c] = e[c];
         bool swapped;
-        s_hdr[b * kMaxTex + k] = quant_bc1_hdr(ep6, swapped);
+        const uint32_t hdr = quant_bc1_hdr(ep6, swapped);
+        s_hdr[b * kMaxTex + k] = hdr;
+        if (NTBC_PACK_PAL) {
+          const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
+          const float e0[3] = {s_unorm[c0 >> 11], s_unorm[32 + ((c0 >> 5) & 63)], s_unorm[c0 & 31]};
+          const float e1[3] = {s_unorm[c1 >> 11], s_unorm[32 + ((c1 >> 5) & 63)], s_unorm[c1 & 31]};
+          bc1_palette_pairs(e0, e1, dst);
+        }
       } else {
         const float ep2[2] = {e[0], e[1]};
-        s_hdr[b * kMaxTex + k] = quant_bc4_hdr(ep2);
+        const uint32_t hdr = quant_bc4_hdr(ep2);
+        s_hdr[b * kMaxTex + k] = hdr;
+        if (NTBC_PACK_PAL) {
+          const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
+          bc4_palette_tab(s_unorm[96 + E0], s_unorm[96 + E1], E0 > E1, s_unorm + 352, dst);
+        }
       }
     }
     __syncthreads();
@@ -500,11 +554,22 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
       const int h = lane >> 4, i = lane & 15, b = min(wb + h, nb - 1);
       const bool valid = wb + h < nb;
       const float* c = s_col + (i >> 2) * rs + (4 * b + (i & 3)) * p.n_c;
-      for (int k = 0; k < p.n_tex; k++) {
+#pragma unroll
+      for (int k = 0; k < NT; k++) {
         const uint32_t hdr = s_hdr[b * kMaxTex + k];
         const int co = p.col_off[k];
         uint64_t word;
-        if (p.fmt[k] == kFmtBC1) {
+        const float* P = s_pal + b * p.pal_stride + p.pal_off[k];
+        if (NTBC_PACK_PAL && p.fmt[k] == kFmtBC1) {
+          const float cc[3] = {c[co], c[co + 1], c[co + 2]};
+          const uint32_t code = bc1_code_pairs(cc, reinterpret_cast<const float2*>(P), (hdr & 0xFFFFu) == (hdr >> 16));
+          word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
+        } else if (NTBC_PACK_PAL) {
+          const float4 q0 = reinterpret_cast<const float4*>(P)[0], q1 = reinterpret_cast<const float4*>(P)[1];
+          const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          const uint32_t code = bc4_code(c[co], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu));
+          word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
+        } else if (p.fmt[k] == kFmtBC1) {
           const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
           const float e0[3] = {s_unorm[c0 >> 11], s_unorm[32 + ((c0 >> 5) & 63)], s_unorm[c0 & 31]};
           const float e1[3] = {s_unorm[c1 >> 11], s_unorm[32 + ((c1 >> 5) & 63)], s_unorm[c1 & 31]};

@@ -554,6 +554,8 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
       const int h = lane >> 4, i = lane & 15, b = min(wb + h, nb - 1);
       const bool valid = wb + h < nb;
       const float* c = s_col + (i >> 2) * rs + (4 * b + (i & 3)) * p.n_c;
+      const bool store = (lane & 15) == 0 && valid;
+      const size_t oidx = (size_t)row * p.BW + bx0 + wb + h;   // texture-independent word index
 #pragma unroll
       for (int k = 0; k < NT; k++) {
         const uint32_t hdr = s_hdr[b * kMaxTex + k];
@@ -581,7 +583,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
           bc4_palette_tab(s_unorm[96 + E0], s_unorm[96 + E1], E0 > E1, s_unorm + 352, pl);
           word = (uint64_t)hdr | (pack_bc4_indices(bc4_code(c[co], pl, E0 > E1), lane) << 16);
         }
-        if ((lane & 15) == 0 && valid) p.out[k][(size_t)row * p.BW + bx0 + wb + h] = word;
+        if (store) p.out[k][oidx] = word;
       }
     }
   }

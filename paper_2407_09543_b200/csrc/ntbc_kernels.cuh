@@ -444,7 +444,10 @@ struct PackParams {
   int pal_off[kMaxTex], pal_stride;   // per block: BC1 12 / BC4 8 palette floats per texture
   uint64_t* out[kMaxTex];
 };
-constexpr int kPackTileBlocks = 64;   // block positions per tile (one block row): 256 texel columns x 4 rows
+#ifndef NTBC_PACK_TILE
+#define NTBC_PACK_TILE 64
+#endif
+constexpr int kPackTileBlocks = NTBC_PACK_TILE;   // block positions per tile (one block row): 4 x kPackTileBlocks texel columns x 4 rows
 
 #ifndef NTBC_PACK_STAGES
 #define NTBC_PACK_STAGES 1      // tile buffers in shared memory: 2 = the next tile's loads overlap this tile's math

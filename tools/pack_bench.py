@@ -52,7 +52,9 @@ def main(tag="r01", steps=20):
            "algorithmic_bytes": nbytes, "median_ms": ms, "min_ms": ts[0], "achieved_gbs": gbs,
            "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)",
-           "words_equal_fused_kernel": same}
+           "words_equal_fused_kernel": same,
+           "bound_note": "SIMT issue (ALU pipe ~61%, 71% issue-active), not HBM: ncu DRAM bytes = the algorithmic "
+                         "bytes (profiles/r01zd_pack_ncu.md), so frac is HBM headroom, not the limiting resource"}
     print(json.dumps(out))
     with open(os.path.join(ROOT, "profiles", f"pack_{tag}.json"), "w") as f:
         json.dump(out, f, indent=1)

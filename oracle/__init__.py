@@ -78,6 +78,8 @@ def lib():
             "o_block_sq_error": (C.c_double, [u64, i32, vp]),
             "o_storage_bytes": (u64, [i32] * 10),
             "o_exp_max_relerr": (C.c_double, [f32, f32, i32, i32]),
+            "o_set_act_model": (None, [i32]),
+            "o_get_act_model": (i32, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -180,6 +182,28 @@ def get_dot_model():
     o = np.zeros(4, np.int32)
     lib().o_get_dot_model(_p(o))
     return tuple(int(x) for x in o)
+
+
+def set_act_model(plain: int):
+    lib().o_set_act_model(int(plain))
+
+
+class plain_definitions:
+    """Context manager: the oracle computes the PLAIN definitions (every dot product exact and rounded
+    once, selu / sigmoid in float64 with libm, one rounding) instead of the pinned op sequences the
+    kernels execute (R9, R10).  The binary16 operand rounding of P:322 / P:331 stays."""
+
+    def __enter__(self):
+        self._dot = get_dot_model()
+        self._act = int(lib().o_get_act_model())
+        set_dot_model(0)
+        set_act_model(1)
+        return self
+
+    def __exit__(self, *exc):
+        set_dot_model(*self._dot)
+        set_act_model(self._act)
+        return False
 
 
 def mlp_raw(weights, biases, x) -> np.ndarray:

@@ -8,6 +8,14 @@
  * only fused multiply-adds are the explicit fmaf() calls written below; every
  * other operation is one IEEE-754 binary32 operation rounded to nearest-even.
  *
+ * Two arithmetic modes.  PINNED (default): the op sequences the CUDA kernels execute bit for bit
+ * -- R9's exponential, R10's tensor-core summation order.  PLAIN (o_set_dot_model(0, ...) +
+ * o_set_act_model(1)): the definitions themselves -- every dot product exact and rounded once,
+ * selu / sigmoid in float64 with libm and rounded once -- the reference the faithfulness tests
+ * (tests/test_faithfulness.py) measure both the pinned oracle and the CUDA path against under
+ * north_star's tolerance rule.  The binary16 operand rounding at every layer input
+ * is part of the method and is the same in both modes.
+ *
  * Parity status per function: every function below is pinned by -m "not gpu"
  * tests.  o_dot's summation ORDER (R10: chunks of 16, window p = 25, round toward zero) is a
  * reading of a passage the paper leaves silent ("half-precision floating points"); the
@@ -170,9 +178,22 @@ float o_dequant(uint8_t q, float s, int32_t z) { return s * (float)((int32_t)q -
 /* ------------------------------------------------------------------------- */
 static const float LOG2E = 0x1.715476p+0f;
 static const float MAGIC = 12582912.0f;                      /* 1.5 * 2^23 */
-/* Q(f) ~ (2^f - 1)/f on |f| <= 1/2, minimax in relative error (<= 1.6e-5: below 1/16 of a binary16
-   ulp, the precision the hidden activations are stored in) */
-static const float Q0 = 0x1.62e2d6p-1f, Q1 = 0x1.ebff08p-3f, Q2 = 0x1.c96b34p-5f, Q3 = 0x1.3b2a76p-7f;
+/* Q(f) ~ (2^f - 1)/f on |f| <= 1/2, minimax in relative error of Q (so that both e^x and the selu
+   branch's e^z - 1 = 2^n (1 + f Q) - 1 keep it, including f -> 0).  Degree 4 (R9 v4): the degree-3
+   polynomial of v3 (|rel| 1.5e-5 = 1/30 of a binary16 ulp) flips the binary16 rounding of ~3% of the
+   hidden activations against the plain definition, and the fp16 re-rounding of every layer input
+    amplifies each flip (tests/test_faithfulness.py: 163 vs 10 mismatched words on 8,192 C2
+   blocks).  Degrees 3 and 5 are kept for that sensitivity study (-DNTBC_QDEG). */
+#ifndef NTBC_QDEG
+#define NTBC_QDEG 4
+#endif
+#if NTBC_QDEG == 3   /* |rel| <= 1.5e-5 */
+static const float QC[4] = {0x1.62e2d6p-1f, 0x1.ebff08p-3f, 0x1.c96b34p-5f, 0x1.3b2a76p-7f};
+#elif NTBC_QDEG == 4 /* |rel| <= 4.7e-7 */
+static const float QC[5] = {0x1.62e42ep-1f, 0x1.ebfa4ep-3f, 0x1.c6b26ep-5f, 0x1.3cbe58p-7f, 0x1.5d87dep-10f};
+#else                /* degree 5, |rel| <= 2.1e-8 */
+static const float QC[6] = {0x1.62e430p-1f, 0x1.ebfbdep-3f, 0x1.c6af6ep-5f, 0x1.3b2ba0p-7f, 0x1.5f07b4p-10f, 0x1.4308fap-13f};
+#endif
 static const float SELU_L = 0x1.0cfabep+0f;                  /* RN32(1.0507009873554804934) */
 static const float SELU_LA = 0x1.c212ccp+0f;                 /* RN32(lambda * alpha)        */
 
@@ -183,7 +204,9 @@ static int exp_reduce(float x, float* f_out, float* q_out) {
     float negnf = MAGIC - r;                      /* -n, exact */
     float f = fmaf(x, LOG2E, negnf);              /* x log2e - n, one rounding */
     *f_out = f;
-    *q_out = fmaf(fmaf(fmaf(Q3, f, Q2), f, Q1), f, Q0);
+    float q = QC[NTBC_QDEG];                      /* Horner, highest coefficient first */
+    for (int i = NTBC_QDEG - 1; i >= 0; i--) q = fmaf(q, f, QC[i]);
+    *q_out = q;
     int32_t ri, mi; memcpy(&ri, &r, 4); float mg = MAGIC; memcpy(&mi, &mg, 4);
     return ri - mi;
 }
@@ -200,27 +223,54 @@ float o_exp(float x) {
     float s = pow2i(n, 1.0f);
     return fmaf(s, f * q, s);
 }
-/* selu negative branch (R8/R9): lambda*alpha*(e^z - 1) = fma(S, RN(1 + f q), -lambda*alpha),
-   S = lambda*alpha*2^n exact */
-static float selu_neg(float z) {
+/* selu negative branch (R8/R9): lambda*alpha*(e^z - 1) = fma(S, RN(f q), S - lambda*alpha),
+   S = lambda*alpha*2^n exact.  For n = 0 the addend S - lambda*alpha is exactly 0, so there is no
+   cancellation as z -> 0^- (the result keeps the polynomial's relative accuracy down to the
+   smallest z; pinned by test_selu_branch_relative_error_near_zero). */
+static float selu_neg_pinned(float z) {
     float x = fmaxf(z, -80.0f), f, q;
     int n = exp_reduce(x, &f, &q);
     float S = pow2i(n, SELU_LA);
-    return fmaf(S, fmaf(f, q, 1.0f), -SELU_LA);
+    return fmaf(S, f * q, S - SELU_LA);
 }
-float o_expm1(float x) { return selu_neg(x) / SELU_LA; }   /* for the accuracy pin only (x <= 0) */
+
+/* ------------------------------------------------------------------------- */
+/* activation model: 0 = the pinned op sequences above (R9, what the kernel computes);          */
+/* 2 = the same in binary32 libm (expm1f / expf; a sensitivity variant, not a reference); */
+/* 1 = the PLAIN definitions (P:332-333 with the standard selu constants): evaluated in  */
+/* float64 with libm exp/expm1 and rounded once to binary32 -- the faithfulness reference.      */
+/* ------------------------------------------------------------------------- */
+static int g_act_plain = 0;
+void o_set_act_model(int plain) { g_act_plain = plain; }
+int  o_get_act_model(void) { return g_act_plain; }
+static const double SELU_LAMBDA_D = 1.0507009873554804934, SELU_ALPHA_D = 1.6732632423543772848;
+
+static float selu_neg(float z) {
+    if (g_act_plain == 2) return SELU_LA * expm1f(z);        /* a binary32 libm variant (sensitivity study) */
+    if (g_act_plain) return (float)(SELU_LAMBDA_D * SELU_ALPHA_D * expm1((double)z));
+    return selu_neg_pinned(z);
+}
+float o_expm1(float x) { return selu_neg_pinned(x) / SELU_LA; }   /* for the accuracy pin only (x <= 0) */
 
 /* selu ([selu] Klambauer et al.): lambda z (z > 0) else lambda alpha (e^z - 1) */
-float o_selu(float z) { return z > 0.0f ? SELU_L * z : selu_neg(z); }
+float o_selu(float z) {
+    if (g_act_plain == 2) return z > 0.0f ? SELU_L * z : selu_neg(z);
+    if (g_act_plain) return z > 0.0f ? (float)(SELU_LAMBDA_D * (double)z) : selu_neg(z);
+    return z > 0.0f ? SELU_L * z : selu_neg(z);
+}
 /* sigmoid: 1 / (1 + e^-z), IEEE division */
-float o_sigmoid(float z) { float d = 1.0f + o_exp(-z); return 1.0f / d; }
+float o_sigmoid(float z) {
+    if (g_act_plain == 2) return 1.0f / (1.0f + expf(-z));
+    if (g_act_plain) return (float)(1.0 / (1.0 + exp(-(double)z)));
+    float d = 1.0f + o_exp(-z); return 1.0f / d;
+}
 
 double o_exp_max_relerr(float lo, float hi, int step, int which) {
     double worst = 0.0;
     float x = lo;
     while (x <= hi) {
         double ref = which == 0 ? exp((double)x) : (double)SELU_LA * expm1((double)x);
-        double got = which == 0 ? (double)o_exp(x) : (double)selu_neg(x);
+        double got = which == 0 ? (double)o_exp(x) : (double)selu_neg_pinned(x);
         double den = fabs(ref);
         if (den > 0) { double e = fabs(got - ref) / den; if (e > worst) worst = e; }
         for (int k = 0; k < step; k++) x = nextafterf(x, INFINITY);

@@ -41,6 +41,9 @@ float    o_exp(float x);                                       /* pinned E, R9 *
 float    o_expm1(float x);                                     /* selu_neg(x)/(lambda alpha), accuracy pin only */
 float    o_selu(float z);                                      /* P:333, R8 */
 float    o_sigmoid(float z);                                   /* P:332, R8 */
+/* activation model: 0 = pinned op sequences (R9, default), 1 = plain float64/libm definitions */
+void     o_set_act_model(int plain);
+int      o_get_act_model(void);
 
 /* Summation model of one layer's dot product (R10).
    mode 0 = CR  : b + sum_k w_k a_k exactly, one RN to fp32.

@@ -84,24 +84,33 @@ def test_dequant_eq2_single_rounding():
 
 
 # ---------------------------------------------------------------- pinned exp (R9), selu / sigmoid
+# The accuracy bound of the pinned exponential is fixed by the paper, not by the implementation:
+# the hidden activations are stored in binary16, so E and the selu branch must stay
+# within 1/16 of a binary16 ulp (relative 2^-15) of the exact function everywhere, including the
+# selu branch as z -> 0^- (no cancellation: its binary16 result must not depend on how E is built).
+# These bounds do not move when the kernel changes.
+BIN16_ULP_16 = 2.0 ** -15
+SELU_LAMBDA, SELU_ALPHA = 1.0507009873554804934, 1.6732632423543772848
+
+
 def test_exp_accuracy_vs_libm():
-    """R9: the degree-3 Q keeps E within 1e-5 of e^x (relative) on the clamp range."""
+    """R9: E(x) within 2^-15 relative of e^x on the whole clamp range (libm exp in float64)."""
     assert L.o_exp(0.0) == 1.0
-    assert L.o_exp_max_relerr(-80.0, 80.0, 100003, 0) < 1e-5
-    assert L.o_exp_max_relerr(-10.0, 10.0, 10007, 0) < 1e-5
-    assert L.o_exp_max_relerr(-80.0, -1e-2, 20011, 1) < 2e-5       # selu's lambda*alpha*(e^z - 1) branch
+    assert L.o_exp_max_relerr(-80.0, 80.0, 100003, 0) < BIN16_ULP_16
+    assert L.o_exp_max_relerr(-10.0, 10.0, 10007, 0) < BIN16_ULP_16
 
 
-def test_selu_branch_error_bound():
-    """R9: lambda alpha (e^z - 1) = fma(S, RN(1 + f q), -lambda alpha) has relative error <= 2e-5 plus an
-    absolute error <= 6e-8 from RN(1 + f q) (below a binary16 subnormal ulp, 2^-24) -- dense in z -> 0^-."""
-    z = -np.concatenate([np.geomspace(1e-30, 80, 40001), np.linspace(1e-4, 20, 40001)]).astype(np.float32)
-    la = float(np.float32(float.fromhex("0x1.c212ccp+0")))
+def test_selu_branch_relative_error_near_zero():
+    """R9: lambda alpha (e^z - 1) within 2^-15 RELATIVE of the exact value (libm expm1, exact
+    constants) for every z in (-80, 0), densely down to z = -1e-38: no cancellation as z -> 0^-."""
+    z = -np.concatenate([np.geomspace(1e-38, 80, 60001), np.linspace(1e-4, 20, 40001)]).astype(np.float32)
     got = np.array([L.o_selu(float(v)) for v in z], np.float64)
-    ref = la * np.expm1(z.astype(np.float64))
-    assert np.all(np.abs(got - ref) <= 2e-5 * np.abs(ref) + 6e-8)
-    assert np.all(got <= 0.0) and np.all(got >= -la)                # monotone range of the branch
-    assert np.all(np.diff(got[:40001]) <= 0.0)                     # non-increasing as z decreases
+    ref = SELU_LAMBDA * SELU_ALPHA * np.expm1(z.astype(np.float64))
+    assert np.max(np.abs(got - ref) / np.abs(ref)) < BIN16_ULP_16
+    la = float(np.float32(SELU_LAMBDA * SELU_ALPHA))
+    assert np.all(got <= 0.0) and np.all(got >= -la)                # range of the branch
+    assert np.all(np.diff(got[:60001]) <= 0.0)                     # non-increasing as z decreases
+    assert L.o_exp_max_relerr(-80.0, -1e-30, 20011, 1) < BIN16_ULP_16
 
 
 def test_selu_sigmoid_vs_torch_float64():
@@ -111,8 +120,10 @@ def test_selu_sigmoid_vs_torch_float64():
     ref_sig = torch.sigmoid(zt).numpy()
     got_selu = np.array([L.o_selu(float(v)) for v in z])
     got_sig = np.array([L.o_sigmoid(float(v)) for v in z])
-    assert np.all(np.abs(got_selu - ref_selu) <= 2e-5 * np.abs(ref_selu) + 6e-8)
-    assert np.max(np.abs(got_sig - ref_sig) / ref_sig) < 1e-5
+    nz = ref_selu != 0
+    assert np.all(got_selu[~nz] == 0.0)
+    assert np.max(np.abs(got_selu[nz] - ref_selu[nz]) / np.abs(ref_selu[nz])) < BIN16_ULP_16
+    assert np.max(np.abs(got_sig - ref_sig) / ref_sig) < BIN16_ULP_16
     assert L.o_selu(0.0) == 0.0 and L.o_sigmoid(0.0) == 0.5
     assert L.o_sigmoid(1e30) == 1.0 and 0.0 <= L.o_sigmoid(-1e30) < 1e-30
 

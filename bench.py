@@ -2,12 +2,13 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
 
-A step = one pass of the whole hot path over one synthetic 4k material
-(config C3: 4096^2, diffuse+normal BC1, roughness+AO+displacement BC4 -- MetalPlates013-shaped),
-i.e. one ntbc_decode_material call (one fused-kernel launch).  Under torchrun (N>1) every rank
-decodes its own material (weak scaling) and the packed BC bytes are gathered to rank 0 with NCCL
-inside the timed region (BASELINE.json north_star: "only a final gather of packed bytes, counted in
-the timing").  Rank 0 prints ONE JSON line.
+A step = one pass of the whole hot path over synthetic 4k materials (config
+C3: 4096^2, diffuse+normal BC1, roughness+AO+displacement BC4 -- MetalPlates013-shaped), one
+ntbc_decode_material call per material (grid dequant launch + fused-kernel launch).  N = 1: one material
+per step (the metric's "ms per 4k material").  N > 1 (torchrun): BASELINE config 5, a batch of 64 C3-shaped
+materials (distinct seeds) sharded 64/N per rank (--materials), every rank's fused kernel storing its BC
+words straight into rank 0's buffer (the final gather of packed bytes, counted in the timing; north_star).
+Rank 0 prints ONE JSON line.
 
 --impl reference times the CPU oracle (the reference arm for this paper-only task)
 on a bounded sample of block rows per step, on this box's host cores.
@@ -31,23 +32,7 @@ METRIC = "BC blocks decoded/sec and ms per 4k material at 1/2/4/8 B200 (% roofli
 UNIT = "Mblocks/s"
 
 
-# ---------------------------------------------------------------- algorithmic work model (DESIGN.md §7.3)
-def ops_per_material(spec, W, H):
-    """Algorithmic element-wise ops of the pinned definitions (R6, R8, R9, R11-R18), excluding the
-    tensor-core contraction: one op per IEEE operation, integer op or conversion."""
-    n_bc1 = sum(1 for f in spec.fmts if f == 1)
-    n_bc4 = len(spec.fmts) - n_bc1
-    # per hidden activation (incl. fp16 cvt, R9 v3), per sigmoid, per grid level and texel (coordinates, floor,
-    # fractions, index, 3 lerps x 2 features, fp16 cvt; the Eq.2 dequantization runs once per vertex in
-    # dequant_grids_kernel since r01w and is not counted per texel)
-    selu, sig, lvl = 18, 16, 22
-    hidden = spec.hidden * spec.n_hidden
-    per_texel = hidden * selu + spec.n_color_out * sig + spec.texel_levels * lvl + 4 + 46 * n_bc1 + 42 * n_bc4
-    per_block = (hidden * selu + spec.n_endpoint_out * sig + spec.block_levels * lvl + 4 + 40 * n_bc1 + 12 * n_bc4)
-    blocks = (W // 4) * (H // 4)
-    return blocks * (16 * per_texel + per_block), per_texel, per_block
-
-
+# ---------------------------------------------------------------- algorithmic work model (SURVEY §8(d), DESIGN.md §7.3)
 def mma_flops_per_material(spec, W, H):
     """Algorithmic MLP FLOPs (2 x MACs of the paper's layers, unpadded)."""
     def macs(dims):
@@ -172,13 +157,51 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------- our arm
+def pack_roofline(model, spec, W, H, dev, peaks, reps=20):
+    """Kernel (2) standalone (ntbc_pack, rows a5-a8 fed the fp32 MLP outputs of the whole C3 material, produced
+    once by ntbc_debug_mlp): HBM roofline.  Algorithmic bytes per launch = the fp32 endpoint + colour outputs
+    read once + the BC words written once."""
+    import torch
+
+    from paper_2407_09543_b200 import ntbc
+    fmts = list(spec.fmts)
+    ep_d, col_d = ntbc.debug_mlp(model, W, H)
+    outs = [torch.empty((H // 4, W // 4), dtype=torch.int64, device=dev) for _ in fmts]
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        ntbc.pack(fmts, ep_d, col_d, W, H, outs=outs)
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ntbc.pack(fmts, ep_d, col_d, W, H, outs=outs)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = sum(ts) / len(ts)
+    nbytes = ep_d.numel() * 4 + col_d.numel() * 4 + len(fmts) * (W // 4) * (H // 4) * 8
+    peak = peaks.get("hbm_gbs", 6556.2)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "latest_pack_traffic.json")))
+        traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return {"kernel": f"pack_kernel<{len(fmts)}>", "bound": "hbm", "achieved": nbytes / (ms * 1e-3) / 1e9,
+            "peak": peak, "unit": "GB/s", "frac": nbytes / (ms * 1e-3) / 1e9 / peak, "traffic": traffic,
+            "bytes_per_launch": nbytes, "kernel_ms": ms,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import synth
     from paper_2407_09543_b200 import ntbc
-    from paper_2407_09543_b200.shard import PeerGather, PeerRows, gather_materials
+    from paper_2407_09543_b200.shard import PeerGather, PeerRows, gather_materials, material_shards
 
     # NTBC_BENCH_ONE_GPU=1: functional check of the multi-rank path on a one-GPU box (every rank on cuda:0,
     # gloo process group; the ranks' kernels never wait on each other).  Its numbers are not measurements.
@@ -187,33 +210,39 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     W, H, spec = synth.config_shape(args.config)
-    blob = synth.model_blob(args.config, material=rank)
-    model = ntbc.Model(blob, local_rank)
-    n_tex = model.n_tex
+    n_mat = args.materials or (1 if world == 1 else 64)
+    lo, hi = material_shards(n_mat, world)[rank]
+    blobs = [synth.model_blob(args.config, material=g) for g in range(lo, hi)]
+    models = [ntbc.Model(b, local_rank) for b in blobs]
+    n_tex = len(spec.fmts)
     BW, BH = W // 4, H // 4
     plane = BH * BW
-    out_all = torch.empty((n_tex, BH, BW), dtype=torch.int64, device=dev)   # contiguous for the gather
-    outs = [out_all[k] for k in range(n_tex)]
+    out_all = torch.empty((max(1, hi - lo), n_tex, BH, BW), dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
     # the final gather of packed bytes to rank 0 (north star), inside the timed step: fused into the decode
     # by default (every rank's kernel stores its BC words into rank 0's buffer over NVLink, PeerGather);
     # NTBC_GATHER=nccl uses a separate NCCL gather after the decode instead
     gather_mode = os.environ.get("NTBC_GATHER", "peer") if world > 1 else "none"
-    pg = PeerGather(n_tex, BH, BW, rank, world, dev) if gather_mode == "peer" else None
+    pg = PeerGather(n_tex, BH, BW, rank, world, dev, n_materials=n_mat) if gather_mode == "peer" else None
     if pg is not None and not pg.ok:   # no IPC / peer access on this system: all ranks fall back together
         print(f"rank {rank}: peer gather unavailable ({pg.error}); using the NCCL gather", file=sys.stderr)
         pg.close()
         pg, gather_mode = None, "nccl"
+    if gather_mode == "nccl" and len({e - b for b, e in material_shards(n_mat, world)}) != 1:
+        raise SystemExit("--materials must be a multiple of the world size for the NCCL gather")
 
     def step():
+        for i, m in enumerate(models):
+            if pg is not None:
+                ntbc.decode_material([m], W, H, out_ptrs=pg.ptrs_of(lo + i), stream=stream)
+            else:
+                ntbc.decode_material([m], W, H, outs=[out_all[i, k] for k in range(n_tex)], stream=stream)
         if pg is not None:
-            ntbc.decode_material([model], W, H, out_ptrs=pg.ptrs, stream=stream)
             pg.complete()
-        else:
-            ntbc.decode_material([model], W, H, outs=outs, stream=stream)
-            if world > 1:
-                gather_materials(out_all, rank, world)
+        elif world > 1:
+            for i in range(hi - lo):
+                gather_materials(out_all[i], rank, world)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -222,26 +251,37 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     launches0 = ntbc.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # the dominant kernel (fused_decode_kernel) timed live inside the timed steps: the library records these
+    # events right before / after each fused launch on the launch stream (ntbc_debug_time_fused); with several
+    # materials per step the pair holds the step's last launch
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in kev:   # torch creates the CUDA events lazily on first record
+        a.record(stream)
+        b.record(stream)
+    torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
-        for s in range(args.steps):
+        for s_ in range(args.steps):
             flush.zero_()                                  # L2 flushed between timed steps (not timed)
-            evs[s][0].record(stream)
+            ntbc.time_fused(*kev[s_])
+            evs[s_][0].record(stream)
             step()
-            evs[s][1].record(stream)
+            evs[s_][1].record(stream)
         torch.cuda.synchronize()
+    ntbc.time_fused(None, None)
     if world > 1:
         dist.barrier()
     launches = ntbc.launch_count() - launches0
-    if pg is not None and rank == 0:   # rank 0's buffer holds every rank's material: spot-check our own slice
-        ntbc.decode_material([model], W, H, outs=outs, stream=stream)
+    if pg is not None and rank == 0:   # rank 0's buffer holds every rank's materials: spot-check our first one
+        ntbc.decode_material([models[0]], W, H, outs=[out_all[0, k] for k in range(n_tex)], stream=stream)
         torch.cuda.synchronize()
-        assert torch.equal(pg.buf[0], out_all), "peer gather: rank 0 slice differs from a local decode"
+        assert torch.equal(pg.buf[lo], out_all[0]), "peer gather: rank 0 slice differs from a local decode"
     times = [a.elapsed_time(b) for a, b in evs]
     t_ms = sum(times) / len(times)
+    k_ms = sum(a.elapsed_time(b) for a, b in kev) / len(kev)
 
     # ---- latency view (N > 1, peer gather): ONE material split by block rows over the ranks, every rank
     # decoding its rows straight into rank 0's buffer; time = max over ranks (the metric's "ms per 4k
-    # material at N GPUs" as a single-material latency, beside the weak-scaling throughput above)
+    # material at N GPUs" as a single-material latency, beside the batch throughput above)
     lat_ms = None
     if pg is not None:
         pr = PeerRows(n_tex, BH, BW, rank, world, dev)
@@ -271,22 +311,13 @@ def run_ours(args, rank, world, local_rank):
                 assert torch.equal(pr.buf, ref), "row-split peer decode differs from a local decode"
         pr.close()
         dist.barrier()
-    t_tensor = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+    t_tensor = torch.tensor([t_ms, k_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
-    t_ms_max = float(t_tensor.item())
+    t_ms_max, k_ms_max = (float(x) for x in t_tensor.tolist())
 
-    # ---- kernel-only timing of the dominant kernel (the fused decode kernel), same stream
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for s in range(args.steps):
-        flush.zero_()
-        kev[s][0].record(stream)
-        ntbc.decode_material([model], W, H, outs=outs, stream=stream)
-        kev[s][1].record(stream)
-    torch.cuda.synchronize()
-    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
-
-    # ---- end to end through the C ABI with host buffers (pinned blob in, pinned BC words out)
+    # ---- end to end through the C ABI with host buffers (pinned blob in, pinned BC words out), per rank
+    model, blob = models[0], blobs[0]
     pinned_blob = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
     host_all = torch.empty((n_tex, BH, BW), dtype=torch.int64).pin_memory()   # one pinned [tex][BH][BW] buffer
     host_out = [host_all[k] for k in range(n_tex)]
@@ -298,7 +329,7 @@ def run_ours(args, rank, world, local_rank):
     e_steps = max(3, min(args.steps, 20))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for s in range(e_steps):
+    for s_ in range(e_steps):
         ntbc.decode_material_host([model], [pinned_blob], W, H, host_out, stream=stream)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -313,9 +344,8 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    blocks_step = plane * n_tex * world
+    blocks_step = plane * n_tex * n_mat
     value = blocks_step / (t_ms_max * 1e-3) / 1e6
-    ops, per_texel, per_block = ops_per_material(spec, W, H)
     clocks = clk.summary()
     peaks = {}
     try:
@@ -323,51 +353,69 @@ def run_ours(args, rank, world, local_rank):
     except Exception:
         pass
     sm_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    sm_now = clocks.get("sm_mhz") or sm_max
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    alu_peak = n_sm * 128 * sm_max * 1e6 / 1e9          # Gop/s: 128 lane-instructions / clk / SM
-    achieved = ops / (k_ms * 1e-3) / 1e9
-    traffic, ncu_ctx = None, None
+    # roofline of the dominant kernel: algorithmic MLP FLOPs per launch (2 x MACs of the paper's
+    # layers, unpadded: 333,824 per C3 block position x 1,048,576 positions) / fused-kernel time, against the
+    # measured dense 16-bit tensor peak (fp16 = bf16 rate on B200; burst figure: the kernel is timed alone)
+    flops = mma_flops_per_material(spec, W, H)
+    t_peak = peaks.get("bf16_tflops", 1691.9)
+    achieved = flops / (k_ms_max * 1e-3) / 1e12
+    traffic, ncu_ctx, issue = None, None, None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "latest_fused_traffic.json")))
         if prof.get("config") == args.config:
             traffic = prof.get("dram_bytes_per_launch")
-            # cross-check of the op-count fraction with hardware counters from the committed ncu capture
             ncu_ctx = {k: prof.get(k) for k in ("source", "issue_active", "alu_pipe", "fma_pipe", "tensor_pipe",
                                                  "thread_instructions_per_texel")}
+            ipt = prof.get("thread_instructions_per_texel")
+            if ipt:
+                # the binding resource: SIMT issue.  SASS thread-instructions per texel (ncu, committed capture)
+                # x texels / (SMs x 128 lanes x SM clock under load x live fused-kernel time)
+                cap = n_sm * 128 * sm_now * 1e6 * k_ms_max * 1e-3
+                issue = {"thread_instructions_per_texel": ipt, "texels": W * H,
+                         "frac": ipt * W * H / cap, "sm_mhz": sm_now,
+                         "definition": "ncu SASS thread-instructions/texel x texels / (SMs x 128 x clock x kernel time)"}
     except Exception:
         pass
+    hbm_bytes = len(blob) + plane * n_tex * 8
+    pack = None
+    if world == 1 and not args.no_pack:
+        pack = pack_roofline(models[0], spec, W, H, dev, peaks)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu, _, _ = oracle_sample(args.config, budget_s=args.cpu_budget)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_ms_max, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t_ms_max, "higher_is_better": True,
+        "scaling": "weak" if n_mat == world else "strong",
         "vs_baseline": None, "dtype": "f16 MMA operands / f32 accumulate+epilogue", "data": "synthetic",
-        "config": {"workload": synth.CONFIGS[args.config]["name"], "width": W, "height": H,
+        "config": {"workload": synth.CONFIGS[args.config]["name"] if n_mat == 1 else
+                   f"C5: batch of {n_mat} x " + synth.CONFIGS[args.config]["name"],
+                   "width": W, "height": H,
                    "textures": len(spec.fmts), "formats": ["BC1" if f == 1 else "BC4" for f in spec.fmts],
                    "model": "paper architecture (P:330-343), random-init seeded weights",
-                   "materials_per_rank_per_step": 1, "gather_to_rank0": world > 1,
+                   "materials_per_step": n_mat, "materials_per_rank": hi - lo, "gather_to_rank0": world > 1,
                    "gather": {"none": None, "peer": "fused: each rank's kernel stores its BC words into rank 0's "
                               "buffer over NVLink (CUDA IPC), completion by a 1-element all-reduce",
                               "nccl": "separate NCCL gather after the decode"}[gather_mode],
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "ms_per_4k_material": t_ms_max / world if world > 1 else t_ms_max,
+                   "ms_per_4k_material": t_ms_max * world / n_mat,
                    "latency_ms_per_4k_material": lat_ms if world > 1 else t_ms_max},
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
-                     "frac": achieved / alu_peak, "traffic": traffic,
-                     "kernel": "fused_decode_kernel", "kernel_ms": k_ms,
-                     "kernel_ms_covers": "CUDA events around ntbc_decode_material: dequant_grids_kernel "
-                                         "(row a2's Eq.2 half, ~1% of the step) + fused_decode_kernel",
-                     "ops_per_texel": per_texel, "ops_per_block": per_block, "ncu": ncu_ctx,
-                     "peak_source": f"{n_sm} SMs x 128 lane-instr/clk x {sm_max:.0f} MHz (DESIGN.md §7.3)",
-                     "tensor": {"achieved_tflops": mma_flops_per_material(spec, W, H) / (k_ms * 1e-3) / 1e12,
-                                "peak_tflops": peaks.get("bf16_tflops", 1658.0),
-                                "frac": mma_flops_per_material(spec, W, H) / (k_ms * 1e-3) / 1e12 /
-                                peaks.get("bf16_tflops", 1658.0)}},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": t_peak, "unit": "TFLOP/s",
+                     "frac": achieved / t_peak, "traffic": traffic,
+                     "kernel": "fused_decode_kernel", "kernel_ms": k_ms_max,
+                     "flops_per_launch": flops, "flops_per_block_position": flops // plane,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; dense fp16 = bf16 rate)",
+                     "issue": issue,
+                     "hbm": {"bytes_per_launch": hbm_bytes, "achieved_gbs": hbm_bytes / (k_ms_max * 1e-3) / 1e9,
+                             "frac": hbm_bytes / (k_ms_max * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6556.2)},
+                     "ncu": ncu_ctx, "pack": pack},
         "cpu_baseline": cpu,
-        "e2e": {"value": blocks_step / (e_ms * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": e_ms,
-                "h2d_bytes_per_step": len(blob), "d2h_bytes_per_step": plane * n_tex * 8,
-                "api": "ntbc_decode_material_host (pinned host blob -> device -> BC words -> pinned host)"},
+        "e2e": {"value": plane * n_tex * world / (e_ms * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": e_ms,
+                "h2d_bytes_per_step": len(blob) * world, "d2h_bytes_per_step": plane * n_tex * 8 * world,
+                "api": "ntbc_decode_material_host (pinned host blob -> device -> BC words -> pinned host), "
+                       "one material per rank per step"},
         "gpu_launches": launches,
         "clocks": clocks,
     }
@@ -382,7 +430,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--materials", type=int, default=None,
+                    help="materials per step over all ranks (default: 1 at N = 1, BASELINE config 5's 64 at N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pack", action="store_true", help="skip the standalone pack kernel's HBM roofline")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

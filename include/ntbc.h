@@ -15,7 +15,12 @@
  *     stream are asynchronous: launch errors are returned, device faults surface at the caller's
  *     next synchronisation of that stream;
  *   - no entry point allocates device memory on the hot path (ntbc_decode_material,
- *     ntbc_decode_bc, ntbc_pack); scratch is owned by the model and sized at load time.
+ *     ntbc_decode_bc, ntbc_pack); scratch is owned by the model and sized at load time;
+ *   - thread safety: any call may be made from any host thread.  Calls that use or change a model
+ *     (decode, upload, debug dumps) are serialised per model on the host, and decodes of one model
+ *     issued on different streams are ordered on the device (each waits for the model's previous
+ *     launch: they share the model's fp32 grid region), so concurrent use of ONE model on several
+ *     streams is correct but not concurrent on the GPU; use one model per stream for overlap.
  * Readings of silent passages are numbered R1..R20 in DESIGN.md §2.
  */
 #ifndef NTBC_H
@@ -33,7 +38,7 @@ typedef enum { NTBC_BC1 = 1, NTBC_BC4 = 4 } ntbc_format; /* PAPER.md:106-115 */
 
 typedef enum {
   NTBC_OK = 0,
-  NTBC_EINVAL = -1,    /* bad argument: NULL, size/alignment/range (W,H % 4, rows, pointers 16-B aligned) */
+  NTBC_EINVAL = -1,    /* bad argument: NULL, size/alignment/range (W,H % 4, rows, pointer alignment) */
   NTBC_EFORMAT = -2,   /* bad .ntbc blob: magic, version, truncation, dims inconsistent with header */
   NTBC_EMISMATCH = -3, /* models vs request (e.g. conservative pair not one all-BC1 + one all-BC4) */
   NTBC_ENOMEM = -4,    /* device allocation failed */
@@ -79,7 +84,9 @@ void ntbc_free_model(ntbc_model m);                     /* NULL ok; caller guara
  *   width, height: texels, multiples of 4, identical for every texture of the material;
  *   [block_row_begin, block_row_end): shard of the H/4 block rows to decode (0 <= begin < end <= H/4);
  *   out_blocks: one device pointer per texture, models[0]'s textures then models[1]'s, each
- *     (end-begin) * (width/4) * 8 bytes, 16-B aligned; row-major little-endian 64-bit BC words:
+ *     (end-begin) * (width/4) * 8 bytes, 8-B aligned (16-B aligned pointers and an even width/4 let
+ *     the kernel write two adjacent blocks' words as one 16-byte store); row-major little-endian
+ *     64-bit BC words:
  *     BC1 = c0 | c1<<16 | sum code_i << (32+2i), BC4 = e0 | e1<<8 | sum code_i << (16+3i), texel i = 4y+x.
  * Errors: NTBC_EINVAL, NTBC_EMISMATCH, NTBC_ECUDA. */
 ntbc_status ntbc_decode_material(const ntbc_model* models, int n_models, int width, int height,
@@ -213,6 +220,13 @@ ntbc_status ntbc_peer_close(void* device_ptr);
 
 /* Number of kernel launches the library issued since load (all entry points), for bench accounting. */
 uint64_t ntbc_launch_count(void);
+
+/* Measurement hook (bench.py's roofline of the dominant kernel): while set, every fused-kernel launch
+ * made by THIS host thread through ntbc_decode_material / ntbc_decode_material_host records
+ * `start_event` right before and `end_event` right after it on the launch stream (cudaEvent_t as
+ * void*, created by the caller with timing enabled).  Pass NULL, NULL to clear.  Not for concurrent
+ * use of the same events.  Errors: NTBC_EINVAL (exactly one of the two is NULL). */
+ntbc_status ntbc_debug_time_fused(void* start_event, void* end_event);
 
 const char* ntbc_last_error(void);                     /* thread-local message of the last failure */
 

@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <map>
+#include <set>
 #include <unordered_map>
 #include <string>
 #include <vector>
@@ -25,6 +27,9 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+// ntbc_debug_time_fused: events recorded on the launch stream right before / after each fused-kernel
+// launch of this host thread (bench.py's roofline timing of the dominant kernel)
+thread_local cudaEvent_t g_time_fused[2] = {nullptr, nullptr};
 
 ntbc_status fail(ntbc_status st, const char* fmt, ...) {
   char buf[512];
@@ -43,6 +48,20 @@ ntbc_status fail(ntbc_status st, const char* fmt, ...) {
   } while (0)
 
 size_t al16(size_t n) { return (n + 15) & ~size_t(15); }
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device context: set it once per (device, kernel),
+// under a lock (several host threads, several devices per process)
+cudaError_t allow_smem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, kern})) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({dev, kern});
+  return e;
+}
 uint32_t rd32(const uint8_t* p) { uint32_t v; memcpy(&v, p, 4); return v; }
 
 // Parsed architecture of a .ntbc blob.  Offsets index the blob.
@@ -156,9 +175,16 @@ constexpr int kCopyStreams = 4;
 struct ntbc_model_s {
   int device;
   Arch arch;
+  // thread safety (include/ntbc.h): every call that launches work on the model or changes it holds `mu`;
+  // decodes of one model on different streams are ordered on the device by `last_done`, recorded after
+  // each launch (they share the model's fp32 grid region, rewritten by every decode's dequant launch)
+  std::recursive_mutex mu;
+  cudaEvent_t last_done = nullptr;
+  cudaStream_t last_stream = nullptr;
   uint8_t* d_blob = nullptr;   // weight slot: the blob, then at fg_base its grids dequantized to fp32
   size_t blob_cap = 0;         // slot bytes
   size_t fg_base = 0;          // offset of the fp32 grids in a slot
+  size_t img_off = 0;          // offset of the fused kernel's shared-memory prefix image in a slot
   // dynamic-scheduling unit counters: a ring of kSchedRing ints, one per launch (zeroed on the
   // launch's stream), so up to kSchedRing launches of this model may be in flight concurrently
   int* d_sched = nullptr;
@@ -231,13 +257,17 @@ ntbc_status dequant_grids(ntbc_model_s* m, cudaStream_t st) {
       const long long res = (long long)a.coarsest[g] << l;
       d.src_off[d.n_levels] = a.level_off[g][l];
       d.dst_off[d.n_levels] = m->fg_base + a.fg_off[g][l];
-      d.end[d.n_levels] = (d.n_levels ? d.end[d.n_levels - 1] : 0) + res * res * 2;
+      d.end[d.n_levels] = (d.n_levels ? d.end[d.n_levels - 1] : 0) + (res * res * 2 + 3) / 4;   // 4-code groups
       d.s[d.n_levels] = a.s[g][l];
       d.z[d.n_levels] = a.z[g][l];
     }
   d.zero_off = m->fg_base + a.fg_zero_off;
   d.zero_n = (int)((a.fg_bytes - a.fg_zero_off) / sizeof(float));
-  const long long total4 = d.end[d.n_levels - 1] / 4;
+  d.net[0] = m->net[0];
+  d.net[1] = m->net[1];
+  d.H = a.hidden;
+  d.img_off = m->img_off;
+  const long long total4 = d.end[d.n_levels - 1];
   const int grid = (int)std::min<long long>((total4 + 255) / 256, 148 * 8);
   dequant_grids_kernel<<<grid, 256, 0, st>>>(d);
   g_launches++;
@@ -252,25 +282,48 @@ struct DevGuard {
 };
 
 template <int H, int NWG, bool DUMP>
-ntbc_status launch_fused_t(const FusedParams& p, size_t smem, int grid, cudaStream_t st) {
-  auto kern = p.naive ? fused_decode_kernel<H, NWG, DUMP, true> : fused_decode_kernel<H, NWG, DUMP, false>;
-  static bool configured[2] = {false, false};  // per instantiation
-  if (!configured[p.naive]) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured[p.naive] = true;
-  }
-  kern<<<grid, NWG * 128, smem, st>>>(p);
+ntbc_status launch_fused_t(const FusedLaunch& L, size_t smem, int grid, cudaStream_t st) {
+  auto kern = L.m[0].naive ? fused_decode_kernel<H, NWG, DUMP, true> : fused_decode_kernel<H, NWG, DUMP, false>;
+  CUDA_TRY(allow_smem((const void*)kern, 227 * 1024));
+  if (!DUMP && g_time_fused[0]) CUDA_TRY(cudaEventRecord(g_time_fused[0], st));
+  kern<<<grid, NWG * 128, smem, st>>>(L);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
+  if (!DUMP && g_time_fused[1]) CUDA_TRY(cudaEventRecord(g_time_fused[1], st));
   return NTBC_OK;
 }
 
 size_t fused_smem(const FusedParams& p, int nwg) {
   return (size_t)p.net[0].img_bytes + p.net[1].img_bytes + kOnesBytes + kUnormBytes +
-         (size_t)nwg * (p.a_bytes + p.pal_bytes) + 8 * nwg + 16 + 4 * 8;
+         (size_t)nwg * (p.a_bytes + p.pal_bytes) + 8 * (nwg + 1) + 16 + 4 * 8;
+}
+
+ntbc_status launch_fused_locked(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st);
+
+// order this launch after the model's previous one when that ran on another stream
+ntbc_status order_after_last(ntbc_model_s* m, cudaStream_t st) {
+  if (m->last_done && m->last_stream != st) CUDA_TRY(cudaStreamWaitEvent(st, m->last_done, 0));
+  return NTBC_OK;
+}
+ntbc_status record_last(ntbc_model_s* m, cudaStream_t st) {
+  if (!m->last_done) CUDA_TRY(cudaEventCreateWithFlags(&m->last_done, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(m->last_done, st));
+  m->last_stream = st;
+  return NTBC_OK;
 }
 
 ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
+  std::lock_guard<std::recursive_mutex> lk(m->mu);
+  ntbc_status s0 = order_after_last(m, st);
+  if (s0) return s0;
+  s0 = launch_fused_locked(m, p, dump, st);
+  if (s0) return s0;
+  return record_last(m, st);
+}
+
+// the grid dequantization + prefix build launch of model m, then every kernel parameter of its half of a
+// fused launch
+ntbc_status prepare_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
   const Arch& a = m->arch;
   ntbc_status dst = dequant_grids(m, st);
   if (dst) return dst;
@@ -279,6 +332,7 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
     CUDA_TRY(cudaMemsetAsync(p.next_unit, 0, sizeof(int), st));
   }
   p.blob = m->d_blob;
+  p.prefix = m->d_blob + m->img_off;
   for (int g = 0; g < 2; g++) {
     p.levels[g] = a.levels[g];
     for (int l = 0; l < a.levels[g]; l++) {
@@ -328,44 +382,72 @@ ntbc_status launch_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_
   p.tpal_off = (uint32_t)((a.n_tex * 128 * (a.naive ? 5 : 4) + 15) & ~15u);   // BC1 swap flags: naive only
   p.pal_bytes = p.tpal_off + (uint32_t)(8 * p.pal_stride * sizeof(float));
   p.naive = a.naive;
+  p.vec16 = (p.BW % 2) == 0;
+  for (int k = 0; k < a.n_tex; k++)
+    if ((uintptr_t)p.out[k] & 15) p.vec16 = 0;
+  return NTBC_OK;
+}
+
+// work groups per CTA: more independent groups per SM hide more latency (C3: NWG 4 -> 2.70 ms, 6 -> 2.65
+// with 8% wave-quantisation loss, 8 -> 2.46) but each group's unit takes ~1.8x longer, so 8 groups pay only
+// with at least two full waves of units (C2, 512 units: NWG 4 = 0.19 ms on 128 SMs in one wave, NWG 8 =
+// 0.34 ms on 64 SMs); 5 and 6 quantise badly on power-of-two unit counts.  One launch runs one model, or
+// the two models of a conservative pair on disjoint CTA ranges (each CTA holds one model's operand images).
+ntbc_status launch_prepared(FusedParams* ps, int n, int hidden, bool dump, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t cap = 227 * 1024;
-  // work groups per CTA: more independent groups per SM hide more latency (C3: NWG 4 -> 2.70 ms,
-  // 6 -> 2.65 with 8% wave-quantisation loss, 8 -> 2.46) but each group's unit takes ~1.8x longer, so
-  // 8 groups pay only with at least two full waves of units (C2, 512 units: NWG 4 = 0.19 ms on 128
-  // SMs in one wave, NWG 8 = 0.34 ms on 64 SMs); 5 and 6 quantise badly on power-of-two unit counts
-  int dev0 = 0, sms0 = 148;
-  cudaGetDevice(&dev0);
-  cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+  int units = 0;
+  for (int i = 0; i < n; i++) units += ps[i].n_units;
+  auto smem_of = [&](int w) { size_t m = 0; for (int i = 0; i < n; i++) m = std::max(m, fused_smem(ps[i], w)); return m; };
   int nwg = 2;
   for (int w : {8, 4, 3})
-    if ((w != 8 || p.n_units >= 2 * 8 * sms0) && fused_smem(p, w) <= cap) { nwg = w; break; }
+    if ((w != 8 || units >= 2 * 8 * sms) && smem_of(w) <= cap) { nwg = w; break; }
   if (const char* e = getenv("NTBC_NWG")) {  // measurement override (bench sweeps); clamped to what fits
     const int want = atoi(e);
-    if ((want >= 2 && want <= 4 || want == 8) && fused_smem(p, want) <= cap) nwg = want;
+    if ((want >= 2 && want <= 4 || want == 8) && smem_of(want) <= cap) nwg = want;
   }
-  const size_t smem = fused_smem(p, nwg);
+  const size_t smem = smem_of(nwg);
   if (smem > cap) return fail(NTBC_EINVAL, "model needs %zu B of shared memory (> %zu)", smem, cap);
-  int grid = (p.n_units + nwg - 1) / nwg;
-  if (grid > sms) grid = sms;
-  if (grid < 1) grid = 1;
+  FusedLaunch L{};
+  L.m[0] = ps[0];
+  L.m[1] = n > 1 ? ps[1] : ps[0];
+  int grid;
+  if (n == 1) {
+    grid = std::max(1, std::min(sms, (ps[0].n_units + nwg - 1) / nwg));
+    L.split = grid;
+  } else {
+    // CTAs in proportion to each model's work: units x (per-texel MLP + per-texture index/pack cost),
+    // measured ~90 SASS instructions per texel per texture against ~2,700 for the MLPs
+    double w[2];
+    for (int i = 0; i < 2; i++) w[i] = ps[i].n_units * (2700.0 + 90.0 * ps[i].n_tex);
+    grid = sms;
+    int split = (int)std::lround(grid * w[0] / (w[0] + w[1]));
+    if (const char* e = getenv("NTBC_PAIR_SPLIT")) split = atoi(e);   // measurement override
+    L.split = std::max(1, std::min(grid - 1, split));
+  }
 #define NTBC_DISPATCH(HH)                                                                        \
-  if (a.hidden == HH) {                                                                          \
-    if (nwg == 8) return dump ? launch_fused_t<HH, 8, true>(p, smem, grid, st)                   \
-                              : launch_fused_t<HH, 8, false>(p, smem, grid, st);                 \
-    if (nwg == 4) return dump ? launch_fused_t<HH, 4, true>(p, smem, grid, st)                   \
-                              : launch_fused_t<HH, 4, false>(p, smem, grid, st);                 \
-    if (nwg == 3) return dump ? launch_fused_t<HH, 3, true>(p, smem, grid, st)                   \
-                              : launch_fused_t<HH, 3, false>(p, smem, grid, st);                 \
-    return dump ? launch_fused_t<HH, 2, true>(p, smem, grid, st) : launch_fused_t<HH, 2, false>(p, smem, grid, st); \
+  if (hidden == HH) {                                                                            \
+    if (nwg == 8) return dump ? launch_fused_t<HH, 8, true>(L, smem, grid, st)                   \
+                              : launch_fused_t<HH, 8, false>(L, smem, grid, st);                 \
+    if (nwg == 4) return dump ? launch_fused_t<HH, 4, true>(L, smem, grid, st)                   \
+                              : launch_fused_t<HH, 4, false>(L, smem, grid, st);                 \
+    if (nwg == 3) return dump ? launch_fused_t<HH, 3, true>(L, smem, grid, st)                   \
+                              : launch_fused_t<HH, 3, false>(L, smem, grid, st);                 \
+    return dump ? launch_fused_t<HH, 2, true>(L, smem, grid, st) : launch_fused_t<HH, 2, false>(L, smem, grid, st); \
   }
   NTBC_DISPATCH(16)
   NTBC_DISPATCH(32)
   NTBC_DISPATCH(64)
 #undef NTBC_DISPATCH
   return fail(NTBC_EINVAL, "unsupported hidden width");
+}
+
+ntbc_status launch_fused_locked(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st) {
+  ntbc_status s0 = prepare_fused(m, p, dump, st);
+  if (s0) return s0;
+  return launch_prepared(&p, 1, m->arch.hidden, dump, st);
 }
 
 // cuStreamWaitValue64 through the runtime's driver entry-point query (no link-time libcuda dependency)
@@ -483,7 +565,8 @@ ntbc_status ntbc_load_model(const void* blob, size_t nbytes, int cuda_device, nt
   m->arch = a;
   layout_nets(m);
   m->fg_base = (al16(nbytes) + 255) & ~size_t(255);
-  m->blob_cap = m->fg_base + a.fg_bytes;
+  m->img_off = (m->fg_base + a.fg_bytes + 255) & ~size_t(255);
+  m->blob_cap = m->img_off + m->net[0].img_bytes + m->net[1].img_bytes + kOnesBytes + kUnormBytes;
   if (cudaMalloc(&m->d_blob, m->blob_cap) != cudaSuccess) {
     cudaGetLastError();
     ntbc_free_model(m);
@@ -504,8 +587,13 @@ ntbc_status ntbc_model_upload_async(ntbc_model m, const void* blob, size_t nbyte
   if (st) return st;
   if (!same_arch(a, m->arch)) return fail(NTBC_EMISMATCH, "blob architecture differs from the loaded model");
   DevGuard dg(m->device);
+  std::lock_guard<std::recursive_mutex> lk(m->mu);
+  st = order_after_last(m, (cudaStream_t)stream);   // the previous decode (any stream) still reads the weights
+  if (st) return st;
   m->arch = a;  // same layout; refresh the per-level (s, z)
-  return upload(m, blob, nbytes, (cudaStream_t)stream);
+  st = upload(m, blob, nbytes, (cudaStream_t)stream);
+  if (st) return st;
+  return record_last(m, (cudaStream_t)stream);
 }
 
 ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out) {
@@ -544,6 +632,7 @@ void ntbc_free_model(ntbc_model m) {
   for (auto& row : m->tlset)
     for (auto e : row) if (e) cudaEventDestroy(e);
   if (m->uploaded) cudaEventDestroy(m->uploaded);
+  if (m->last_done) cudaEventDestroy(m->last_done);
   if (m->upload_stream) cudaStreamDestroy(m->upload_stream);
   cudaFree(m->slot_blob[1]);
   delete m;
@@ -563,17 +652,46 @@ ntbc_status ntbc_decode_material(const ntbc_model* models, int n_models, int wid
       return fail(NTBC_EMISMATCH, "conservative pair must be one all-BC1 and one all-BC4 model");
     if (models[0]->device != models[1]->device) return fail(NTBC_EMISMATCH, "models on different devices");
   }
+  FusedParams ps[2] = {};
   int t = 0;
   for (int i = 0; i < n_models; i++) {
-    ntbc_model_s* m = models[i];
-    DevGuard dg(m->device);
-    FusedParams p{};
+    FusedParams& p = ps[i];
     p.W = width; p.H = height; p.row_begin = r0; p.row_end = r1;
-    for (int k = 0; k < m->arch.n_tex; k++, t++) {
-      if (!out_blocks[t] || ((uintptr_t)out_blocks[t] & 15)) return fail(NTBC_EINVAL, "out_blocks[%d] NULL or not 16-B aligned", t);
+    for (int k = 0; k < models[i]->arch.n_tex; k++, t++) {
+      if (!out_blocks[t] || ((uintptr_t)out_blocks[t] & 7)) return fail(NTBC_EINVAL, "out_blocks[%d] NULL or not 8-B aligned", t);
       p.out[k] = (uint64_t*)out_blocks[t];
     }
-    st = launch_fused(m, p, false, (cudaStream_t)stream);
+  }
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (n_models == 1 || models[0]->arch.hidden != models[1]->arch.hidden || models[0]->arch.naive != models[1]->arch.naive ||
+      (getenv("NTBC_PAIR_LAUNCHES") && atoi(getenv("NTBC_PAIR_LAUNCHES")))) {
+    for (int i = 0; i < n_models; i++) {   // one fused launch per model
+      DevGuard dg(models[i]->device);
+      st = launch_fused(models[i], ps[i], false, cs);
+      if (st) return st;
+    }
+    return NTBC_OK;
+  }
+  // conservative pair in ONE persistent launch: both models' prep launches, then one fused kernel whose
+  // CTAs are partitioned by model (f1)
+  DevGuard dg(models[0]->device);
+  ntbc_model_s* lk0 = models[0] < models[1] ? models[0] : models[1];   // fixed lock order
+  ntbc_model_s* lk1 = models[0] < models[1] ? models[1] : models[0];
+  std::lock_guard<std::recursive_mutex> g0(lk0->mu);
+  std::unique_lock<std::recursive_mutex> g1(lk1->mu, std::defer_lock);
+  if (lk1 != lk0) g1.lock();
+  for (int i = 0; i < 2; i++) {
+    st = order_after_last(models[i], cs);
+    if (st) return st;
+  }
+  for (int i = 0; i < 2; i++) {
+    st = prepare_fused(models[i], ps[i], false, cs);
+    if (st) return st;
+  }
+  st = launch_prepared(ps, 2, models[0]->arch.hidden, false, cs);
+  if (st) return st;
+  for (int i = 0; i < 2; i++) {
+    st = record_last(models[i], cs);
     if (st) return st;
   }
   return NTBC_OK;
@@ -601,6 +719,7 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
     ntbc_model_s* m = models[i];
     if (!m) return fail(NTBC_EINVAL, "model %d is NULL", i);
     DevGuard dg(m->device);
+    std::lock_guard<std::recursive_mutex> lk(m->mu);   // the call swaps the model's weight slot
     const int n_tex = m->arch.n_tex;
     for (int k = 0; k < n_tex; k++)
       if (!host_out[t + k]) return fail(NTBC_EINVAL, "host_out[%d] is NULL", t + k);
@@ -698,11 +817,17 @@ ntbc_status ntbc_decode_material_host(const ntbc_model* models, int n_models, co
       for (int k = 0; k < n_tex; k++)
         CUDA_TRY(cudaMemcpyAsync(host_out[t + k], p.out[k], plane, cudaMemcpyDeviceToHost, cs));
     } else {
-      // chunk c's copies wait until all units of chunk c have been published by the running kernel
+      // the launched kernel publishes every chunk: advance all targets first, so an error below cannot
+      // leave later chunks' targets one call behind the device counters
       for (int c = 0; c < n_chunks; c++) {
         int r0, r1;
         chunk_rows(c, r0, r1);
         m->progress_target[c] += (unsigned long long)(r1 - r0) * upr;
+      }
+      // chunk c's copies wait until all units of chunk c have been published by the running kernel
+      for (int c = 0; c < n_chunks; c++) {
+        int r0, r1;
+        chunk_rows(c, r0, r1);
         // the last chunk finishes with the kernel: copy it in stream order right behind the kernel
         // (no counter wait, whose latency would add to the exposed tail)
         const bool last = c == n_chunks - 1 && n_chunks > 1;
@@ -832,8 +957,19 @@ ntbc_status train_step(int net, const ntbc_train_arch* arch, float* params, floa
   CUDA_TRY(cudaMemsetAsync(loss, 0, sizeof(float), st));
   p.qsz = nullptr;
   if (arch->qat) {   // QAT: per-level min/max -> (s, z) of the 8-bit fake quantizer, on the GPU
-    static thread_local int* d_q = nullptr;   // [2*kMaxLevels] ordered-int min/max, then [2*kMaxLevels] (s, z)
-    if (!d_q && cudaMalloc(&d_q, 4 * kMaxLevels * sizeof(int)) != cudaSuccess) { cudaGetLastError(); d_q = nullptr; return fail(NTBC_ENOMEM, "QAT scratch"); }
+    // [2*kMaxLevels] ordered-int min/max, then [2*kMaxLevels] (s, z): one scratch per (device, stream), so
+    // steps on other devices or concurrent streams never share it
+    static std::mutex q_mu;
+    static std::map<std::pair<int, cudaStream_t>, int*> q_scratch;
+    int q_dev = 0;
+    cudaGetDevice(&q_dev);
+    int* d_q = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(q_mu);
+      int*& slot = q_scratch[{q_dev, st}];
+      if (!slot && cudaMalloc(&slot, 4 * kMaxLevels * sizeof(int)) != cudaSuccess) { cudaGetLastError(); slot = nullptr; return fail(NTBC_ENOMEM, "QAT scratch"); }
+      d_q = slot;
+    }
     int init[2 * kMaxLevels];
     for (int l = 0; l < kMaxLevels; l++) { init[2 * l] = 0x7FFFFFFF; init[2 * l + 1] = (int)0x80000000; }
     CUDA_TRY(cudaMemcpyAsync(d_q, init, sizeof(init), cudaMemcpyHostToDevice, st));
@@ -856,11 +992,7 @@ ntbc_status train_step(int net, const ntbc_train_arch* arch, float* params, floa
   smem += al4((size_t)kTrainTile * (2 * p.levels + 1)) + 4 * (size_t)kTrainTile * (64 + 4) + kTrainTile;
   smem *= sizeof(float);
   auto kern = net == 1 ? train_step_kernel<64, 1> : train_step_kernel<64, 0>;
-  static bool configured[2] = {false, false};
-  if (!configured[net]) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured[net] = true;
-  }
+  CUDA_TRY(allow_smem((const void*)kern, 227 * 1024));
   kern<<<(batch + kTrainTile - 1) / kTrainTile, kTrainTile * kTrainQ, smem, st>>>(p);
   g_launches++;
   const double bc1 = 1.0 - std::pow(0.9, step), bc2 = 1.0 - std::pow(0.999, step);
@@ -948,6 +1080,9 @@ ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const 
     p.pal_stride += fmts[k] == NTBC_BC1 ? 12 : 8;
   }
   p.n_e = eo; p.n_c = co;
+  p.vec16 = (p.BW % 2) == 0;
+  for (int k = 0; k < n_tex; k++)
+    if ((uintptr_t)p.out[k] & 15) p.vec16 = 0;
   p.tiles_per_row = (p.BW + kPackTileBlocks - 1) / kPackTileBlocks;
   p.n_tiles = p.tiles_per_row * p.rows;
   const size_t smem = (384 + (size_t)kPackStages * (4 * (4 * kPackTileBlocks * p.n_c + 4) +
@@ -961,11 +1096,7 @@ ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const 
                                                        pack_kernel<5>, pack_kernel<6>, pack_kernel<7>, pack_kernel<8>};
   static_assert(kMaxTex == 8, "pack kernel instantiations");
   const auto kern = kernels[n_tex - 1];
-  static bool pack_configured[kMaxTex] = {};
-  if (!pack_configured[n_tex - 1]) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    pack_configured[n_tex - 1] = true;
-  }
+  CUDA_TRY(allow_smem((const void*)kern, 227 * 1024));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPackThreads, smem));
   // persistent grid: exactly the resident CTAs (a second partial wave of grid-stride CTAs would double
   // the tail), each striding over 16-block tiles
@@ -981,11 +1112,7 @@ ntbc_status ntbc_debug_mma(const void* A, const void* B, const float* C, float* 
   if (!A || !B || !D) return fail(NTBC_EINVAL, "NULL argument");
   if (K <= 0 || K % 16 || K > 128 || (N != 16 && N != 32 && N != 64)) return fail(NTBC_EINVAL, "bad K=%d N=%d", K, N);
   const size_t smem = 128 * K * 2 + 64 * K * 2 + 64;
-  static bool configured = false;
-  if (!configured) {
-    CUDA_TRY(cudaFuncSetAttribute(mma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
-  }
+  CUDA_TRY(allow_smem((const void*)mma_probe_kernel, 227 * 1024));
   mma_probe_kernel<<<1, 128, smem, (cudaStream_t)stream>>>((const __half*)A, (const __half*)B, C, D, K, N);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
@@ -993,6 +1120,13 @@ ntbc_status ntbc_debug_mma(const void* A, const void* B, const float* C, float* 
 }
 
 uint64_t ntbc_launch_count(void) { return g_launches.load(); }
+
+ntbc_status ntbc_debug_time_fused(void* start_event, void* end_event) {
+  if ((start_event == nullptr) != (end_event == nullptr)) return fail(NTBC_EINVAL, "pass both events or neither");
+  g_time_fused[0] = (cudaEvent_t)start_event;
+  g_time_fused[1] = (cudaEvent_t)end_event;
+  return NTBC_OK;
+}
 
 ntbc_status ntbc_peer_export(const void* device_ptr, void* handle_out) {
   if (!device_ptr || !handle_out) return fail(NTBC_EINVAL, "NULL argument");

@@ -40,6 +40,7 @@ struct NetLayout {
 
 struct FusedParams {
   const uint8_t* blob;    // device copy of the .ntbc blob (grid payloads are read from here)
+  const uint8_t* prefix;  // the shared-memory prefix image built by dequant_grids_kernel (16-B aligned)
   GridLevel lv[2][kMaxLevels];
   int levels[2];
   NetLayout net[2];
@@ -59,6 +60,15 @@ struct FusedParams {
   int pal_off[kMaxTex];         // per texture: float offset of its palette in a block's palette record
   int pal_stride;               // floats per block palette record (BC1 12, BC4 8 per texture)
   uint32_t tpal_off;            // byte offset of the colour tile's palettes inside a work group's region
+  int vec16;                    // every out pointer 16-B aligned and BW even: a warp's two adjacent blocks'
+                                // words leave as one 16-byte store (else one 8-byte store per block)
+};
+
+// One fused launch: CTAs [0, split) run model m[0], CTAs [split, grid) run m[1] (the conservative pair,
+// P:377-381, in one persistent launch; each CTA holds only its own model's operand images).
+struct FusedLaunch {
+  FusedParams m[2];
+  int split;
 };
 
 // ---------------------------------------------------------------- a2 at model upload: Eq.2 dequantization
@@ -69,20 +79,69 @@ struct DequantParams {
   uint8_t* slot;                    // weight slot: blob at 0, fp32 grids at dst_off
   int n_levels;                     // block-grid levels then texel-grid levels (<= 2 x kMaxLevels)
   unsigned long long src_off[2 * kMaxLevels], dst_off[2 * kMaxLevels];
-  long long end[2 * kMaxLevels];    // cumulative code count (res^2 x 2) through level i
+  long long end[2 * kMaxLevels];    // cumulative count of 4-code groups, ceil(res^2 x 2 / 4), through level i
   float s[2 * kMaxLevels];
   int z[2 * kMaxLevels];
   unsigned long long zero_off;      // zero block (unused levels read it)
   int zero_n;
+  // the fused kernel's shared-memory prefix, built here in global memory (img_off in the slot) and
+  // bulk-copied by every CTA's prologue (TMA engine): both nets' tcgen05 B-operand images, the ones tile
+  // of the bias MMA, the UNORM expansion tables and BC4 weights -- byte for byte the smem layout
+  NetLayout net[2];
+  int H;
+  unsigned long long img_off;
 };
-// four codes per thread (level sizes res^2 x 2 and all offsets are multiples of 16 bytes): one 4-byte
-// load, one 16-byte store
+// The shared-memory prefix of the fused kernel: per net and layer the tcgen05 B operand
+// B[N_pad][K_in16 + 16] (row n = output n, K-major core-matrix layout, bias at k = K_in16, read against
+// the ones tile), then the ones tile (one 8-row group, column 0 = 1.0), then the exact UNORM quotients
+// q/31, q/63, q/255 (R12, R13) and the BC4 interpolation weights.  Written with generic stores by
+// threads [tid0, tid0 + nthr) of whoever calls it (the prep kernel into global memory).
+__device__ __forceinline__ uint32_t prefix_bytes(const NetLayout* net) {
+  return net[0].img_bytes + net[1].img_bytes + kOnesBytes + kUnormBytes;
+}
+__device__ inline void build_smem_prefix(uint8_t* dst0, const uint8_t* blob, const NetLayout* net, int H, int tid0,
+                                         int nthr) {
+  uint8_t* img = dst0;
+  for (int n = 0; n < 2; n++) {
+    for (int l = 0; l < 4; l++) {
+      const NetLayout& L = net[n];
+      const int kin = L.kin[l], nout = L.nout[l], kin16 = l == 0 ? 16 : H, npad = l < 3 ? H : L.n_out16;
+      const int K_B = kin16 + 16;
+      const __half* W = reinterpret_cast<const __half*>(blob + L.w_off[l]);
+      const __half* bias = reinterpret_cast<const __half*>(blob + L.b_off[l]);
+      uint8_t* dst = img + L.layer_off[l];
+      for (int t = tid0; t < npad * K_B; t += nthr) {
+        const int k = t / npad, o = t - k * npad;   // o fastest: coalesced reads of W[k][o]
+        __half v = __ushort_as_half((unsigned short)0);
+        if (o < nout && k < kin) v = W[(size_t)k * nout + o];
+        else if (o < nout && k == kin16) v = bias[o];
+        *reinterpret_cast<__half*>(dst + kmajor_offset(o, k, K_B)) = v;
+      }
+    }
+    img += net[n].img_bytes;
+  }
+  if (tid0 < 8) {  // the constant ones tile used to fold the bias into the MMA (all 16 row groups read it)
+    const uint4 c0 = make_uint4(0x3C00u, 0u, 0u, 0u), z = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(img + kmajor_offset(tid0, 0, 16)) = c0;
+    *reinterpret_cast<uint4*>(img + kmajor_offset(tid0, 8, 16)) = z;
+  }
+  float* unorm = reinterpret_cast<float*>(img + kOnesBytes);
+  for (int i = tid0; i < 352; i += nthr)  // UNORM expansion tables: the exact quotients of R12/R13
+    unorm[i] = i < 32 ? __fdiv_rn((float)i, 31.0f) : i < 96 ? __fdiv_rn((float)(i - 32), 63.0f)
+                                                             : __fdiv_rn((float)(i - 96), 255.0f);
+  for (int i = tid0; i < 32; i += nthr) unorm[352 + i] = bc4_weight(i);   // BC4 interpolation weights per mode
+}
+
+// four codes per thread: one 4-byte load, one 16-byte store.  A level whose code count res^2 x 2 is not a
+// multiple of 4 (odd coarsest resolution) ends with a partial group: its extra codes come from the 16-B
+// padding that follows every level in the blob and land in the 16-B padding of the level's fp32 region
+// (never read), so every level starts a fresh group.
 __global__ void __launch_bounds__(256) dequant_grids_kernel(const __grid_constant__ DequantParams d) {
-  const long long total4 = d.end[d.n_levels - 1] / 4;
+  const long long total4 = d.end[d.n_levels - 1];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += (long long)gridDim.x * blockDim.x) {
     int l = 0;
-    while (4 * i >= d.end[l]) l++;
-    const long long j = i - (l ? d.end[l - 1] / 4 : 0);
+    while (i >= d.end[l]) l++;
+    const long long j = i - (l ? d.end[l - 1] : 0);
     const uint32_t q4 = __ldg(reinterpret_cast<const uint32_t*>(d.slot + d.src_off[l]) + j);
     const float s = d.s[l];
     const int z = d.z[l];
@@ -92,6 +151,8 @@ __global__ void __launch_bounds__(256) dequant_grids_kernel(const __grid_constan
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.zero_n; i += gridDim.x * blockDim.x)
     reinterpret_cast<float*>(d.slot + d.zero_off)[i] = 0.0f;
+  build_smem_prefix(d.slot + d.img_off, d.slot, d.net, d.H, blockIdx.x * blockDim.x + threadIdx.x,
+                    gridDim.x * blockDim.x);
 }
 
 // ---------------------------------------------------------------- a1-a2: coordinates + grid encode
@@ -156,8 +217,11 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, in
 // hide more of the dependent epilogue latency.  Units are claimed from a global
 // counter (dynamic scheduling) so they finish in row order (pipelined copy-back, ntbc_api.cu).
 template <int H, int NWG, bool DUMP, bool NAIVE>
-__global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
+__global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid_constant__ FusedLaunch L) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  const int sel = (int)blockIdx.x >= L.split;          // which model this CTA decodes
+  const FusedParams& p = L.m[sel];
+  const int cta = (int)blockIdx.x - (sel ? L.split : 0), ncta = sel ? (int)gridDim.x - L.split : L.split;
   const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5, lane = tid & 31;
 
   // ---- carve shared memory
@@ -173,48 +237,24 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   float* tpal = reinterpret_cast<float*>(wg_base + p.a_bytes + p.tpal_off);   // [8 blocks][pal_stride] colour tile palettes
   uint64_t* bars = reinterpret_cast<uint64_t*>(ones + kOnesBytes + kUnormBytes + NWG * (p.a_bytes + p.pal_bytes));
   uint64_t* bar_mma = bars + wg;                                  // this work group's MMA completion
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG + 1);
   int* next_slot = reinterpret_cast<int*>(tmem_slot + 1) + wg;    // dynamic scheduling: this group's next unit
 
+  // ---- the shared-memory prefix (operand images of both nets, ones tile, UNORM tables), prebuilt in global
+  //      memory by the prep kernel: one bulk asynchronous copy (TMA engine) per 32 KB, completing on bar_img
+  uint64_t* bar_img = bars + NWG;
   if (tid == 0) {
-    for (int g = 0; g < NWG; g++) mbar_init(bars + g, 1);
+    for (int g = 0; g <= NWG; g++) mbar_init(bars + g, 1);
     fence_mbar_init();
+    const uint32_t total = prefix_bytes(p.net);
+    mbar_arrive_expect_tx(bar_img, total);
+    for (uint32_t o = 0; o < total; o += 32768u)
+      bulk_g2s(smem + o, p.prefix + o, min(32768u, total - o), bar_img);
   }
   if (warp == 0) tmem_alloc(tmem_slot, NWG <= 2 ? 128 : NWG <= 4 ? 256 : 512);
-
-  // ---- operand images of both nets, built from the blob's row-major fp16 weights: row n of layer l's
-  //      B operand = output n, K-major core-matrix layout, bias at k = kin16 (read against the ones tile)
-#pragma unroll 1
-  for (int n = 0; n < 2; n++) {
-    uint8_t* img = n == 0 ? img_e : img_c;
-#pragma unroll 1
-    for (int l = 0; l < 4; l++) {
-      const NetLayout& L = p.net[n];
-      const int kin = L.kin[l], nout = L.nout[l], kin16 = l == 0 ? 16 : H, npad = l < 3 ? H : L.n_out16;
-      const int K_B = kin16 + 16;
-      const __half* W = reinterpret_cast<const __half*>(p.blob + L.w_off[l]);
-      const __half* bias = reinterpret_cast<const __half*>(p.blob + L.b_off[l]);
-      uint8_t* dst = img + L.layer_off[l];
-      for (int t = tid; t < npad * K_B; t += NWG * 128) {
-        const int k = t / npad, o = t - k * npad;   // o fastest: coalesced reads of W[k][o]
-        __half v = __ushort_as_half((unsigned short)0);
-        if (o < nout && k < kin) v = W[(size_t)k * nout + o];
-        else if (o < nout && k == kin16) v = bias[o];
-        *reinterpret_cast<__half*>(dst + kmajor_offset(o, k, K_B)) = v;
-      }
-    }
-  }
-  if (tid < 8) {  // the constant ones tile used to fold the bias into the MMA (all 16 row groups read it)
-    const uint4 c0 = make_uint4(0x3C00u, 0u, 0u, 0u), z = make_uint4(0u, 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(ones + kmajor_offset(tid, 0, 16)) = c0;
-    *reinterpret_cast<uint4*>(ones + kmajor_offset(tid, 8, 16)) = z;
-  }
-  for (int i = tid; i < 352; i += NWG * 128)  // UNORM expansion tables: the exact quotients of R12/R13
-    unorm[i] = i < 32 ? __fdiv_rn((float)i, 31.0f) : i < 96 ? __fdiv_rn((float)(i - 32), 63.0f)
-                                                             : __fdiv_rn((float)(i - 96), 255.0f);
-  if (tid < 32) unorm[352 + tid] = bc4_weight(tid);   // BC4 interpolation weights per mode
-  fence_async_smem();
   __syncthreads();
+  mbar_wait(bar_img, 0);   // the copy's writes are visible to this thread (generic reads of the tables) and to
+                           // the tensor core (async-proxy reads of the operand images)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -307,7 +347,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   };
 
 #pragma unroll 1
-  for (int u = blockIdx.x * NWG + wg; u < p.n_units;) {
+  for (int u = cta * NWG + wg; u < p.n_units;) {
     const int by = p.row_begin + u / p.units_per_row;
     const int bx0 = (u % p.units_per_row) * kUnitBlocks;
     const int nvalid = min(kUnitBlocks, p.BW - bx0);
@@ -317,7 +357,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     named_bar_sync(bar_id, 128);  // previous tile's readers of A / staging / headers are done
     // dynamic scheduling (p.next_unit): claim the group's next unit now; it is read at the end of this
     // unit, after the MLP's barriers have ordered the store before every reader
-    if (p.next_unit && r == 0) *next_slot = atomicAdd(p.next_unit, 1) + (int)gridDim.x * NWG;
+    if (p.next_unit && r == 0) *next_slot = atomicAdd(p.next_unit, 1) + ncta * NWG;
     {
       const float s = __fdiv_rn(__fadd_rn((float)min(bx0 + r, p.BW - 1), 0.5f), (float)p.BW);
       const float t = __fdiv_rn(__fadd_rn((float)by, 0.5f), (float)p.BH);
@@ -381,10 +421,15 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           for (int ch = 0; ch < p.net[1].n_out; ch++)
             p.dump_col[(((size_t)(y - 4 * p.row_begin)) * p.W + x) * p.net[1].n_out + ch] = stage[ch * 128 + r];
       } else {
+        // lane 0 of each warp writes the words of the warp's two adjacent blocks (b, b + 1; bx even) as one
+        // 16-byte store when p.vec16, else lanes 0 and 16 write one 8-byte word each
+        const bool pair = p.vec16 && lane == 0 && b + 1 < nvalid;
+        const bool single = p.vec16 ? (lane == 0 && b + 1 >= nvalid && b < nvalid) : ((lane & 15) == 0 && b < nvalid);
         for (int k = 0; k < p.n_tex; k++) {
           const int co = p.col_off[k];
           const uint32_t hdr = hdrs[k * 128 + b];
-          uint64_t word;
+          uint64_t idx[2];
+          int shift;
           if (NAIVE) {  // naive approach: nearest palette weight to the predicted weight
             const float w = stage[co * 128 + r];
             if (p.fmt[k] == kFmtBC1) {
@@ -392,26 +437,30 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
               uint32_t n = naive_bc1_index(w);
               if (swp[k * 128 + b]) n = 3u - n;                  // weights follow the predicted endpoint order
               const uint32_t code = c0 == c1 ? 0u : (0x1320u >> (4 * n)) & 3u;   // linear n -> code [0,2,3,1]
-              word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
+              pack_bc1_indices2(code, lane, idx);
+              shift = 32;
             } else {
               const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
               const uint32_t n = naive_bc4_index(w, E0 > E1, unorm + 352);
               const uint32_t map = E0 > E1 ? 0x17654320u : 0x71543206u;
-              word = (uint64_t)hdr | (pack_bc4_indices((map >> (4 * n)) & 7u, lane) << 16);
+              pack_bc4_indices2((map >> (4 * n)) & 7u, lane, idx);
+              shift = 16;
             }
           } else if (p.fmt[k] == kFmtBC1) {  // the block's palette (precomputed at the tile start)
             const float2* P = reinterpret_cast<const float2*>(tpal + (r >> 4) * p.pal_stride + p.pal_off[k]);
             const float c[3] = {stage[co * 128 + r], stage[(co + 1) * 128 + r], stage[(co + 2) * 128 + r]};
-            const uint32_t code = bc1_code_pairs(c, P, (hdr & 0xFFFFu) == (hdr >> 16));
-            word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
+            pack_bc1_indices2(bc1_code_pairs(c, P, (hdr & 0xFFFFu) == (hdr >> 16)), lane, idx);
+            shift = 32;
           } else {
             const float4* P = reinterpret_cast<const float4*>(tpal + (r >> 4) * p.pal_stride + p.pal_off[k]);
             const float4 q0 = P[0], q1 = P[1];
             const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-            const uint32_t code = bc4_code(stage[co * 128 + r], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu));
-            word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
+            pack_bc4_indices2(bc4_code(stage[co * 128 + r], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu)), lane, idx);
+            shift = 16;
           }
-          if ((lane & 15) == 0 && b < nvalid) p.out[k][out_row + bx] = word;
+          uint64_t* dst = p.out[k] + out_row + bx;
+          if (pair) st_words2(dst, (uint64_t)hdr | (idx[0] << shift), (uint64_t)hdrs[k * 128 + b + 1] | (idx[1] << shift));
+          else if (single) *dst = (uint64_t)hdr | ((lane < 16 ? idx[0] : idx[1]) << shift);
         }
       }
     }
@@ -425,7 +474,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
         atomicAdd(p.progress + chunk, 1ull);
       }
     }
-    u = p.next_unit ? *next_slot : u + (int)gridDim.x * NWG;
+    u = p.next_unit ? *next_slot : u + ncta * NWG;
   }
 
   // the BC-word writers (lanes 0 and 16) order their stores at system scope before the kernel ends: the
@@ -443,6 +492,7 @@ struct PackParams {
   int fmt[kMaxTex], ep_off[kMaxTex], col_off[kMaxTex];
   int pal_off[kMaxTex], pal_stride;   // per block: BC1 12 / BC4 8 palette floats per texture
   uint64_t* out[kMaxTex];
+  int vec16;   // every out pointer 16-B aligned and BW even: two adjacent blocks' words per 16-byte store
 };
 #ifndef NTBC_PACK_TILE
 #define NTBC_PACK_TILE 64
@@ -557,36 +607,43 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
       const int h = lane >> 4, i = lane & 15, b = min(wb + h, nb - 1);
       const bool valid = wb + h < nb;
       const float* c = s_col + (i >> 2) * rs + (4 * b + (i & 3)) * p.n_c;
-      const bool store = (lane & 15) == 0 && valid;
-      const size_t oidx = (size_t)row * p.BW + bx0 + wb + h;   // texture-independent word index
+      // lane 0 writes both blocks' words as one 16-byte store (p.vec16; wb is even), else lanes 0 / 16
+      const bool pair = p.vec16 && lane == 0 && wb + 1 < nb;
+      const bool single = p.vec16 ? (lane == 0 && wb + 1 >= nb) : ((lane & 15) == 0 && valid);
+      const size_t oidx = (size_t)row * p.BW + bx0 + wb + (p.vec16 ? 0 : h);   // texture-independent word index
 #pragma unroll
       for (int k = 0; k < NT; k++) {
         const uint32_t hdr = s_hdr[b * kMaxTex + k];
         const int co = p.col_off[k];
-        uint64_t word;
+        uint64_t idx[2];
+        int shift;
         const float* P = s_pal + b * p.pal_stride + p.pal_off[k];
         if (NTBC_PACK_PAL && p.fmt[k] == kFmtBC1) {
           const float cc[3] = {c[co], c[co + 1], c[co + 2]};
-          const uint32_t code = bc1_code_pairs(cc, reinterpret_cast<const float2*>(P), (hdr & 0xFFFFu) == (hdr >> 16));
-          word = (uint64_t)hdr | (pack_bc1_indices(code, lane) << 32);
+          pack_bc1_indices2(bc1_code_pairs(cc, reinterpret_cast<const float2*>(P), (hdr & 0xFFFFu) == (hdr >> 16)), lane, idx);
+          shift = 32;
         } else if (NTBC_PACK_PAL) {
           const float4 q0 = reinterpret_cast<const float4*>(P)[0], q1 = reinterpret_cast<const float4*>(P)[1];
           const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-          const uint32_t code = bc4_code(c[co], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu));
-          word = (uint64_t)hdr | (pack_bc4_indices(code, lane) << 16);
+          pack_bc4_indices2(bc4_code(c[co], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu)), lane, idx);
+          shift = 16;
         } else if (p.fmt[k] == kFmtBC1) {
           const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
           const float e0[3] = {s_unorm[c0 >> 11], s_unorm[32 + ((c0 >> 5) & 63)], s_unorm[c0 & 31]};
           const float e1[3] = {s_unorm[c1 >> 11], s_unorm[32 + ((c1 >> 5) & 63)], s_unorm[c1 & 31]};
           const float cc[3] = {c[co], c[co + 1], c[co + 2]};
-          word = (uint64_t)hdr | (pack_bc1_indices(bc1_code(cc, e0, e1, c0 == c1), lane) << 32);
+          pack_bc1_indices2(bc1_code(cc, e0, e1, c0 == c1), lane, idx);
+          shift = 32;
         } else {
           const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
           float pl[8];
           bc4_palette_tab(s_unorm[96 + E0], s_unorm[96 + E1], E0 > E1, s_unorm + 352, pl);
-          word = (uint64_t)hdr | (pack_bc4_indices(bc4_code(c[co], pl, E0 > E1), lane) << 16);
+          pack_bc4_indices2(bc4_code(c[co], pl, E0 > E1), lane, idx);
+          shift = 16;
         }
-        if (store) p.out[k][oidx] = word;
+        if (pair) st_words2(p.out[k] + oidx, (uint64_t)hdr | (idx[0] << shift),
+                            (uint64_t)s_hdr[(b + 1) * kMaxTex + k] | (idx[1] << shift));
+        else if (single) p.out[k][oidx] = (uint64_t)hdr | ((lane < 16 ? idx[0] : idx[1]) << shift);
       }
     }
   }

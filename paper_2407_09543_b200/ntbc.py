@@ -56,6 +56,7 @@ _SIGS = {
     "ntbc_peer_open": (_i, [_vp, _i, C.POINTER(_vp)]),
     "ntbc_peer_close": (_i, [_vp]),
     "ntbc_launch_count": (C.c_uint64, []),
+    "ntbc_debug_time_fused": (_i, [_vp, _vp]),
     "ntbc_last_error": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -309,3 +310,11 @@ def peer_close(ptr: int):
 
 def launch_count() -> int:
     return int(_lib.ntbc_launch_count())
+
+
+def time_fused(start_event=None, end_event=None):
+    """ntbc_debug_time_fused: record torch.cuda.Event `start_event` / `end_event` right before / after every
+    fused-kernel launch of this thread (None, None clears)."""
+    a = start_event.cuda_event if start_event is not None else None
+    b = end_event.cuda_event if end_event is not None else None
+    _check(_lib.ntbc_debug_time_fused(a, b))

@@ -113,22 +113,31 @@ class _PeerBuffer:
 
 
 class PeerGather(_PeerBuffer):
-    """Fused gather of one [n_tex, BH, BW] material per rank into rank 0's [world, n_tex, BH, BW] buffer
-    (throughput view: weak scaling over materials).  Every rank decodes straight into its slice
-    (ntbc.decode_material(..., out_ptrs=self.ptrs)); `complete()` is the only exchange on the timed path,
-    after which rank 0's buffer holds all materials (the writes are system-scope fenced by the fused
-    kernel)."""
+    """Fused gather of a batch of equally-shaped materials into rank 0's [n_materials, n_tex, BH, BW] buffer
+    (throughput view; BASELINE config 5: 64 materials sharded 64/G per rank).  Rank r owns the contiguous
+    materials `material_shards(n_materials, world)[r]` and decodes material g straight into its slice
+    (ntbc.decode_material(..., out_ptrs=self.ptrs_of(g))); `complete()` is the only exchange on the timed
+    path, after which rank 0's buffer holds all materials (the writes are system-scope fenced by the fused
+    kernel).  n_materials defaults to one per rank; `ptrs` = the pointers of this rank's first material."""
 
-    def __init__(self, n_tex: int, bh: int, bw: int, rank: int, world: int, device: torch.device, group=None):
-        super().__init__((world, n_tex, bh, bw), rank, world, device, group)
-        plane = bh * bw * 8
-        self.ptrs = [self.base + (rank * n_tex + k) * plane for k in range(n_tex)] if self.ok else None
+    def __init__(self, n_tex: int, bh: int, bw: int, rank: int, world: int, device: torch.device, group=None,
+                 n_materials: int | None = None):
+        n_materials = world if n_materials is None else n_materials
+        super().__init__((n_materials, n_tex, bh, bw), rank, world, device, group)
+        self.n_tex, self.plane = n_tex, bh * bw * 8
+        self.lo, self.hi = material_shards(n_materials, world)[rank]
+        self.ptrs = self.ptrs_of(self.lo) if self.ok and self.hi > self.lo else None
+
+    def ptrs_of(self, g: int):
+        """Device pointers (this rank's address space) of material g's texture planes in rank 0's buffer."""
+        return [self.base + (g * self.n_tex + k) * self.plane for k in range(self.n_tex)]
 
 
 class PeerRows(_PeerBuffer):
     """One material split by block rows over the ranks (latency view): rank r decodes the rows
     row_shards(BH, world)[r] straight into those rows of rank 0's [n_tex, BH, BW] buffer
-    (ntbc.decode_material(..., row_begin=self.r0, row_end=self.r1, out_ptrs=self.ptrs))."""
+    (ntbc.decode_material(..., row_begin=self.r0, row_end=self.r1, out_ptrs=self.ptrs)).  With an odd
+    BW the row offsets are only 8-B aligned; the kernel then writes one 8-byte word per block."""
 
     def __init__(self, n_tex: int, bh: int, bw: int, rank: int, world: int, device: torch.device, group=None):
         super().__init__((n_tex, bh, bw), rank, world, device, group)

@@ -160,6 +160,24 @@ def random_model(spec: ModelSpec, seed: int) -> Model:
     return m
 
 
+def mirrored_model(spec: ModelSpec, seed: int, axis: str) -> Model:
+    """random_model with every grid level's codes mirror-symmetric along `axis` ('x': q[j][i] =
+    q[j][res-1-i]; 'y': q[j][i] = q[res-1-j][i]) and not along the other, and every level's scale
+    s = 2^-6 (dyadic values, so the lattice coordinates and lerps of power-of-two textures are exact).
+    Input of the coordinate / texel-placement symmetry pins (tests/test_oracle.py)."""
+    m = random_model(spec, seed)
+    for grid in (m.block_grid, m.texel_grid):
+        for li, (s_, z, codes) in enumerate(grid):
+            c = codes.copy()
+            res = c.shape[0]
+            if axis == "x":
+                c[:, res - res // 2:] = c[:, :res // 2][:, ::-1]
+            else:
+                c[res - res // 2:] = c[:res // 2][::-1]
+            grid[li] = (np.float32(2.0 ** -6), z, np.ascontiguousarray(c))
+    return m
+
+
 def serialize(m: Model) -> bytes:
     """Write the `.ntbc` v1 container (layout in DESIGN.md §3)."""
     sp = m.spec

@@ -371,3 +371,98 @@ def test_psnr_agreement(ntbc):
         g = ntbc.decode_bc(outs[k], f, W, H).cpu().numpy()
         o = oracle.decode_bc(ref[k], f, W, H)
         assert abs(oracle.psnr(g, tex) - oracle.psnr(o, tex)) <= 0.01
+
+
+@pytest.mark.parametrize("axis", ["x", "y"])
+def test_coordinates_mirror_symmetry(ntbc, axis):
+    """Row a1 and the texel placement on the GPU (R1, R2; tests/test_oracle.py's pin): grids mirror-symmetric
+    along one axis only give mirror-symmetric words, equal to the oracle's."""
+    import test_oracle as T
+    fmts = [synth.BC1, synth.BC4, synth.BC1]
+    blob = synth.serialize(synth.mirrored_model(synth.ModelSpec(fmts, **T.SYM_SPEC), 11, axis))
+    outs = ntbc.decode_material([ntbc.Model(blob)], 64, 64)
+    words = [u64(t) for t in outs]
+    ref = oracle.Model(blob).decode_material(64, 64)
+    for k in range(len(fmts)):
+        assert np.array_equal(words[k], ref[k])
+    assert T.check_mirror(words, fmts, axis) == (3 * 16 * 16, 0)
+
+
+def _digest_record(cfg):
+    import hashlib
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "full_material_digests.json")
+    rec = json.load(open(path)).get(str(cfg)) if os.path.exists(path) else None
+    if rec is None:
+        pytest.skip(f"no oracle digests for C{cfg} (tools/gen_golden_digests.py)")
+    assert rec["model_sha256"] == hashlib.sha256(synth.model_blob(cfg)).hexdigest(), "synthetic model drifted"
+    return rec
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 6])
+def test_full_material_digests(ntbc, cfg):
+    """Every BC word of the full-size 4k materials (C3: 5.24 M words, C4: 8.39 M, C3': 6.29 M) against the
+    oracle, through digests of the oracle's words per 64-row chunk and texture written by
+    tools/gen_golden_digests.py (oracle/ + synth/ only), in the launch configuration bench.py times."""
+    import hashlib
+    rec = _digest_record(cfg)
+    W, H = rec["width"], rec["height"]
+    m = ntbc.Model(synth.model_blob(cfg))
+    outs = [u64(t) for t in ntbc.decode_material([m], W, H)]
+    bad = []
+    for c, chunk in enumerate(rec["chunks"]):
+        r0 = c * rec["chunk_rows"]
+        for k, d in enumerate(chunk):
+            got = hashlib.sha256(outs[k][r0:r0 + rec["chunk_rows"]].astype("<u8").tobytes()).hexdigest()
+            if got != d:
+                bad.append((c, k))
+    n_words = sum(o.size for o in outs)
+    print(f"\nC{cfg}: {n_words} words in {len(rec['chunks'])} x {len(outs)} chunks, {len(bad)} chunks differ")
+    assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_psnr_agreement_full_size(ntbc, cfg):
+    """Decoded PSNR of every texture of the full material (north_star: within 0.01 dB): the GPU decoder
+    (kernel 3) on the GPU's words against the oracle decoder on the oracle's words (C2: the oracle decodes
+    the full material; C3: the oracle's words are the digest-verified GPU words, test_full_material_digests)."""
+    W, H, _ = synth.config_shape(cfg)
+    blob = synth.model_blob(cfg)
+    m = ntbc.Model(blob)
+    outs = ntbc.decode_material([m], W, H)
+    if cfg == 2:
+        ref = oracle.Model(blob).decode_material(W, H)
+    else:
+        import hashlib
+        rec = _digest_record(cfg)
+        ref = [u64(t) for t in outs]
+        for c, chunk in enumerate(rec["chunks"]):
+            r0 = c * rec["chunk_rows"]
+            for k, d in enumerate(chunk):
+                assert hashlib.sha256(ref[k][r0:r0 + rec["chunk_rows"]].astype("<u8").tobytes()).hexdigest() == d
+    for k, f in enumerate(m.fmts):
+        tex = synth.texture(W, H, 3 if f == 1 else 1, seed=100 + k)
+        g = ntbc.decode_bc(outs[k], f, W, H).cpu().numpy()
+        o = oracle.decode_bc(ref[k], f, W, H)
+        pg, po = oracle.psnr(g, tex), oracle.psnr(o, tex)
+        print(f"\nC{cfg} texture {k}: PSNR GPU {pg:.4f} dB, oracle {po:.4f} dB")
+        assert abs(pg - po) <= 0.01
+
+
+@pytest.mark.parametrize("block_coarsest,texel_coarsest", [(3, 5), (5, 3), (7, 9)])
+def test_odd_coarsest_resolutions(ntbc, block_coarsest, texel_coarsest):
+    """Grids whose level code counts res^2 x 2 are not multiples of 4 (odd coarsest resolution): the grid
+    dequantization starts every level on a fresh 4-code group; features and words equal the
+    oracle's."""
+    sp = synth.ModelSpec([synth.BC1, synth.BC4], hidden=32, block_levels=3, block_coarsest=block_coarsest,
+                         texel_levels=4, texel_coarsest=texel_coarsest)
+    blob = synth.serialize(synth.random_model(sp, block_coarsest * 10 + texel_coarsest))
+    W, H = 4 * 130, 4 * 9
+    check_material(ntbc, blob, W, H, [(0, H // 4)])
+    m, om = ntbc.Model(blob), oracle.Model(blob)
+    bf, tf = (t.cpu().numpy() for t in ntbc.debug_features(m, W, H, 0, 2))
+    for bx in (0, 1, 77, 129):
+        s_ = np.float32((np.float32(bx) + np.float32(0.5)) / np.float32(W // 4))
+        t = np.float32(np.float32(1.5) / np.float32(H // 4))
+        assert np.array_equal(bf[1, bx, :6].view(np.uint32), om.grid_encode(0, float(s_), float(t)).view(np.uint32))

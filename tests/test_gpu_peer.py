@@ -66,6 +66,59 @@ def test_peer_gather_two_processes_one_gpu(tmp_path):
         assert bool(np.load(tmp_path / f"eq{r}.npy")[0]), f"rank {r}'s material differs in rank 0's buffer"
 
 
+def _worker_batch(rank, world, port, outdir):
+    """C5-style batch (4 materials, 2 per rank, each decoded into its slice of rank 0's buffer) and the
+    latency view (one material split by block rows, BW odd so shard offsets are only 8-B aligned)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2407_09543_b200 import ntbc
+    from paper_2407_09543_b200.shard import PeerGather, PeerRows
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    W, H = 4 * 251, 4 * 37                      # BW = 251 (odd), BH = 37 (uneven row shards)
+    n_mat = 4
+    tex = ntbc.Model(synth.model_blob(CFG, material=0), 0).n_tex
+    pg = PeerGather(tex, H // 4, W // 4, rank, world, dev, n_materials=n_mat)
+    for g in range(pg.lo, pg.hi):
+        m = ntbc.Model(synth.model_blob(CFG, material=10 + g), 0)
+        ntbc.decode_material([m], W, H, out_ptrs=pg.ptrs_of(g))
+    pg.complete()
+    pr = PeerRows(tex, H // 4, W // 4, rank, world, dev)
+    m0 = ntbc.Model(synth.model_blob(CFG, material=99), 0)
+    ntbc.decode_material([m0], W, H, row_begin=pr.r0, row_end=pr.r1, out_ptrs=pr.ptrs)
+    pr.complete()
+    if rank == 0:
+        ok = []
+        for g in range(n_mat):
+            ref = torch.stack(ntbc.decode_material([ntbc.Model(synth.model_blob(CFG, material=10 + g), 0)], W, H))
+            torch.cuda.synchronize()
+            ok.append(bool(torch.equal(pg.buf[g], ref)))
+        ref = torch.stack(ntbc.decode_material([m0], W, H))
+        torch.cuda.synchronize()
+        ok.append(bool(torch.equal(pr.buf, ref)))
+        np.save(os.path.join(outdir, "batch.npy"), np.array(ok))
+    dist.barrier()
+    pg.close()
+    pr.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_gather_batch_and_row_split_two_processes(tmp_path):
+    import numpy as np
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker_batch, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    ok = np.load(tmp_path / "batch.npy")
+    assert ok.all(), ok
+
+
 def test_peer_handle_offset_and_errors():
     import torch
 

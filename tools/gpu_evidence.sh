@@ -1,19 +1,24 @@
-# GPU-box evidence run: GPU tests, bench line (ours + reference arm), torchrun N=1 path, ncu launch list,
-# ncu --set full capture of the fused kernel.  usage (via gpurun): bash tools/gpu_evidence.sh <tag> [skip_tests]
+# GPU-box evidence run: GPU tests (with the printed faithfulness / digest / PSNR lines), bench line (ours +
+# reference arm + torchrun N=1 path), ncu launch list, ncu --set full captures of the fused kernel and the
+# pack kernel.  usage (via gpurun): bash tools/gpu_evidence.sh <tag> [skip_tests]
 tag=${1:-x}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${tag}_smi.txt 2>&1
+nproc > gpurun_out/${tag}_nproc.txt; lscpu | grep "Model name" >> gpurun_out/${tag}_nproc.txt
 if [ -z "$2" ]; then
-  timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_gpu_tests.log 2>&1; echo "tests exit $?" >> gpurun_out/${tag}_gpu_tests.log
+  timeout 1800 python -m pytest tests -m gpu -q -s -p no:cacheprovider > gpurun_out/${tag}_gpu_tests.log 2>&1; echo "tests exit $?" >> gpurun_out/${tag}_gpu_tests.log
+  cp gpurun_out/faithfulness_gpu.json gpurun_out/${tag}_faithfulness_gpu.json 2>/dev/null
 fi
-timeout 600 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
+timeout 900 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${tag}_bench_ref.json 2> gpurun_out/${tag}_bench_ref.err
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
-  bench.py --gpus 1 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/${tag}_bench_torchrun.json 2> gpurun_out/${tag}_bench_torchrun.err
+  bench.py --gpus 1 --steps 10 --warmup 3 --no-cpu-baseline --no-pack > gpurun_out/${tag}_bench_torchrun.json 2> gpurun_out/${tag}_bench_torchrun.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${tag}_launches.csv \
-  python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${tag}_ncu_launch.log 2>&1
+  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-pack > gpurun_out/${tag}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_decode -c 1 -o gpurun_out/${tag} \
   python tools/profile_step.py 3 2 > gpurun_out/${tag}_ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pack_kernel -c 1 -o gpurun_out/${tag}_pack \
+  python tools/pack_bench.py ${tag} 2 > gpurun_out/${tag}_ncu_pack.log 2>&1
 python tools/tab1.py ${tag} 20 > gpurun_out/${tag}_tab1.log 2>&1; cp profiles/tab1_${tag}.json gpurun_out/
 python tools/pack_bench.py ${tag} 20 > gpurun_out/${tag}_pack.log 2>&1; cp profiles/pack_${tag}.json gpurun_out/
 ls -la gpurun_out

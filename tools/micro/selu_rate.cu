@@ -1,0 +1,118 @@
+// Throughput of variants of the selu pair (bc_device.cuh selu2_h2) on sm_100a: clocks per warp-pair per
+// SMSP with many independent chains (what bounds the hidden-layer epilogue).
+#include <cstdio>
+#include <cstdint>
+#include "../../paper_2407_09543_b200/csrc/bc_device.cuh"
+#define CH 8
+#define ITERS 1024
+using namespace ntbc;
+template <int V>
+__device__ __forceinline__ uint32_t selu_v(float z0, float z1) {
+  const uint64_t L2E = f2pack(0x1.715476p+0f, 0x1.715476p+0f), MG = f2pack(NTBC_MAGIC, NTBC_MAGIC);
+  const uint64_t x = (V == 1) ? f2pack(z0, z1) : f2pack(fmaxf(z0, -80.0f), fmaxf(z1, -80.0f));
+  const uint64_t r = fma2(x, L2E, MG);
+  const uint64_t f = fma2(x, L2E, sub2(MG, r));
+  uint64_t q;
+  if (V == 3) q = fma2(f2pack(NTBC_Q3, NTBC_Q3), f, f2pack(NTBC_Q2, NTBC_Q2));
+  else { q = fma2(f2pack(NTBC_Q4, NTBC_Q4), f, f2pack(NTBC_Q3, NTBC_Q3)); q = fma2(q, f, f2pack(NTBC_Q2, NTBC_Q2)); }
+  q = fma2(q, f, f2pack(NTBC_Q1, NTBC_Q1));
+  q = fma2(q, f, f2pack(NTBC_Q0, NTBC_Q0));
+  const uint64_t u = mul2(f, q);
+  float r0, r1;
+  f2unpack(r, r0, r1);
+  const uint32_t c = (uint32_t)__float_as_int(NTBC_SELU_LA) - ((uint32_t)__float_as_int(NTBC_MAGIC) << 23);
+  const uint64_t S = f2pack(__uint_as_float(((uint32_t)__float_as_int(r0) << 23) + c), __uint_as_float(((uint32_t)__float_as_int(r1) << 23) + c));
+  const uint64_t neg = fma2(S, u, sub2(S, f2pack(NTBC_SELU_LA, NTBC_SELU_LA)));
+  float n0, n1, p0, p1;
+  f2unpack(neg, n0, n1);
+  uint32_t hn;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hn) : "f"(n1), "f"(n0));
+  if (V == 2) return hn;
+  const uint64_t pos = mul2(f2pack(NTBC_SELU_L, NTBC_SELU_L), f2pack(z0, z1));
+  f2unpack(pos, p0, p1);
+  uint32_t hp, m, h;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hp) : "f"(p1), "f"(p0));
+  asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(m) : "r"(__float_as_uint(z0)), "r"(__float_as_uint(z1)));
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(h) : "r"(hn), "r"(hp), "r"(m));
+  return h;
+}
+// V = 4: 2^n from MUFU.EX2 of the (integer) -(MG - r), S = lambda alpha 2^n by FMUL2, no clamp (ex2 of a
+// very negative n flushes to +0, so S = 0 and the branch returns -lambda alpha exactly)
+__device__ __forceinline__ uint32_t selu_mufu(float z0, float z1) {
+  const uint64_t L2E = f2pack(0x1.715476p+0f, 0x1.715476p+0f), MG = f2pack(NTBC_MAGIC, NTBC_MAGIC);
+  const uint64_t x = f2pack(z0, z1);
+  const uint64_t r = fma2(x, L2E, MG);
+  const uint64_t mn = sub2(MG, r);                 // -n, exact
+  const uint64_t f = fma2(x, L2E, mn);
+  uint64_t q = fma2(f2pack(NTBC_Q4, NTBC_Q4), f, f2pack(NTBC_Q3, NTBC_Q3));
+  q = fma2(q, f, f2pack(NTBC_Q2, NTBC_Q2));
+  q = fma2(q, f, f2pack(NTBC_Q1, NTBC_Q1));
+  q = fma2(q, f, f2pack(NTBC_Q0, NTBC_Q0));
+  const uint64_t u = mul2(f, q);
+  float m0, m1, p0_, p1_;
+  f2unpack(mn, m0, m1);
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0_) : "f"(-m0));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1_) : "f"(-m1));
+  const uint64_t S = mul2(f2pack(p0_, p1_), f2pack(NTBC_SELU_LA, NTBC_SELU_LA));
+  const uint64_t neg = fma2(S, u, sub2(S, f2pack(NTBC_SELU_LA, NTBC_SELU_LA)));
+  float n0, n1, p0, p1;
+  f2unpack(neg, n0, n1);
+  const uint64_t pos = mul2(f2pack(NTBC_SELU_L, NTBC_SELU_L), f2pack(z0, z1));
+  f2unpack(pos, p0, p1);
+  uint32_t hn, hp, m, h;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hn) : "f"(n1), "f"(n0));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hp) : "f"(p1), "f"(p0));
+  asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(m) : "r"(__float_as_uint(z0)), "r"(__float_as_uint(z1)));
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(h) : "r"(hn), "r"(hp), "r"(m));
+  return h;
+}
+template <int V>
+__global__ void k(float* out, int seed, long long* cyc) {
+  float a[CH], b[CH];
+  uint32_t h[CH];
+  for (int i = 0; i < CH; i++) { a[i] = -0.3f * (threadIdx.x & 7) - i * 0.01f - seed; b[i] = 0.2f * i - 1.0f; h[i] = 0; }
+  __syncthreads();
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int i = 0; i < CH; i++) {
+      uint32_t s = V == 9 ? selu2_h2(a[i], b[i]) : V == 4 ? selu_mufu(a[i], b[i]) : selu_v<V>(a[i], b[i]);
+      h[i] ^= s;
+      a[i] = __uint_as_float(__float_as_uint(a[i]) ^ (s & 0x10u));   // data dependence (ALU ops)
+      b[i] = __uint_as_float(__float_as_uint(b[i]) ^ (s & 0x100000u));
+    }
+  }
+  long long t1 = clock64();
+  float s = 0; for (int i = 0; i < CH; i++) s += a[i] + b[i] + __uint_as_float(h[i]);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+template <int V>
+void run(const char* name, int warps) {
+  float* o; long long* c; cudaMalloc(&o, 148 * 1024 * 4); cudaMallocManaged(&c, 8);
+  k<V><<<148, warps * 32>>>(o, 1, c); cudaDeviceSynchronize();
+  k<V><<<148, warps * 32>>>(o, 1, c); cudaDeviceSynchronize();
+  const double n = (double)ITERS * CH * warps / 4;
+  printf("%-34s warps/SM %2d: %.2f clk per selu pair per SMSP\n", name, warps, *c / n);
+  cudaFree(o); cudaFree(c);
+}
+__global__ void ex2_int_check(int* bad) {
+  const int n = (int)threadIdx.x - 200;   // n in [-200, 55]
+  float p;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p) : "f"((float)n));
+  const float want = n < -126 ? 0.0f : ldexpf(1.0f, n);
+  if (__float_as_uint(p) != __float_as_uint(want)) atomicAdd(bad, 1);
+  float q;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(q) : "f"(-(float)(-n)));
+  if (__float_as_uint(q) != __float_as_uint(want)) atomicAdd(bad + 1, 1);
+}
+int main() {
+  { int* b; cudaMallocManaged(&b, 8); b[0] = b[1] = 0; ex2_int_check<<<1, 256>>>(b); cudaDeviceSynchronize();
+    printf("ex2.approx.ftz of integers -200..55: %d / %d mismatches vs exact 2^n (0 below 2^-126)\n", b[0], b[1]); }
+  for (int w : {16, 32}) {
+    run<9>("selu2_h2 (library)", w); run<0>("v4 copy", w); run<1>("no clamp", w); run<2>("neg only (no select/pos)", w);
+    run<3>("degree 3", w); run<4>("MUFU 2^n, no clamp", w);
+  }
+  return 0;
+}

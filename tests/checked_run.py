@@ -48,11 +48,12 @@ def main():
             assert np.array_equal(g[r0:r1], ref[k]), (w, hh, k)
             h.update(g.tobytes())
         # a row shard into 8-B aligned planes (8-byte stores)
-        part = torch.zeros((m.n_tex, r1 - r0, w // 4 + 1), dtype=torch.int64, device="cuda")
+        part = torch.zeros((m.n_tex, (r1 - r0) * (w // 4) + 2), dtype=torch.int64, device="cuda")
         ntbc.decode_material([m], w, hh, row_begin=r0, row_end=r1,
                              out_ptrs=[part[k].data_ptr() + 8 for k in range(m.n_tex)])
         for k in range(m.n_tex):
-            assert np.array_equal(u64(part[k])[:, 1:], ref[k]), ("shard", w, hh, k)
+            got = u64(part[k])[1:1 + (r1 - r0) * (w // 4)].reshape(r1 - r0, w // 4)
+            assert np.array_equal(got, ref[k]), ("shard", w, hh, k)
     # conservative pair (one launch, CTAs partitioned by model)
     rgb = synth.serialize(synth.random_model(synth.ModelSpec([synth.BC1, synth.BC1], block_levels=4, texel_levels=5), 5))
     sc = synth.serialize(synth.random_model(synth.ModelSpec([synth.BC4] * 4, block_levels=4, texel_levels=5), 6))

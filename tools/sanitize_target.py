@@ -34,7 +34,7 @@ def main(cfgs):
         ep, col = ntbc.debug_mlp(m, W, H, 0, min(H // 4, 8))
         ntbc.debug_features(m, W, H, 0, 2)
         r0, r1 = 1, min(H // 4, 6)                                 # a shard with an odd row offset
-        part = torch.zeros((m.n_tex, r1 - r0, W // 4 + 1), dtype=torch.int64, device=DEV)
+        part = torch.zeros((m.n_tex, (r1 - r0) * (W // 4) + 2), dtype=torch.int64, device=DEV)
         ntbc.decode_material([m], W, H, row_begin=r0, row_end=r1,
                              out_ptrs=[part[k].data_ptr() + 8 for k in range(m.n_tex)])   # 8-B aligned planes
         ref = oracle.Model(blob).decode_material(W, H, 0, min(H // 4, 8))

@@ -1087,7 +1087,8 @@ ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const 
   p.n_tiles = p.tiles_per_row * p.rows;
   const size_t smem = (384 + (size_t)kPackStages * (4 * (4 * kPackTileBlocks * p.n_c + 4) +
                                                     ((kPackTileBlocks * p.n_e + 3) & ~3)) +
-                       (NTBC_PACK_PAL ? (size_t)kPackTileBlocks * p.pal_stride : 0)) * sizeof(float) +
+                       (NTBC_PACK_PAL == 1 ? (size_t)kPackTileBlocks * p.pal_stride : 0) +
+                       (NTBC_PACK_PAL == 2 ? (size_t)(kPackThreads / 32) * 2 * p.pal_stride : 0)) * sizeof(float) +
                       kPackTileBlocks * kMaxTex * sizeof(uint32_t);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);

@@ -543,7 +543,12 @@ constexpr int kPackTileBlocks = NTBC_PACK_TILE;   // block positions per tile (o
 #define NTBC_PACK_STAGES 1      // tile buffers in shared memory: 2 = the next tile's loads overlap this tile's math
 #endif
 #ifndef NTBC_PACK_PAL
-#define NTBC_PACK_PAL 0         // 1 = palettes built once per block in shared memory (measured slower)
+#define NTBC_PACK_PAL 0         // 0 = palette rebuilt per texel from the header; 1 = once per block for the whole
+                                // tile in shared memory (+12 KB per CTA, measured slower: occupancy 5 -> 3 CTAs);
+                                // 2 = once per block by the lanes of the warp that owns it, into a per-warp
+                                // scratch of 2 x pal_stride floats (measured slower, r02f: 0.427 vs 0.410 ms --
+                                // one lane per (block, texture) diverges on the format and indexes the
+                                // parameter bank at run time)
 #endif
 #ifndef NTBC_PACK_THREADS
 #define NTBC_PACK_THREADS 256
@@ -592,14 +597,15 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
   const int rs = 4 * kPackTileBlocks * p.n_c + 4;         // texel-row stride (+4 floats: rows start 4 banks apart)
   const int stage_floats = 4 * rs + ((kPackTileBlocks * p.n_e + 3) & ~3);
   float* s_pal = psm + 384 + kPackStages * stage_floats;                                   // [64][pal_stride]
-  uint32_t* s_hdr = reinterpret_cast<uint32_t*>(s_pal + (NTBC_PACK_PAL ? kPackTileBlocks * p.pal_stride : 0));   // [64][kMaxTex]
+  uint32_t* s_hdr = reinterpret_cast<uint32_t*>(s_pal + (NTBC_PACK_PAL == 1 ? kPackTileBlocks * p.pal_stride : 0));   // [64][kMaxTex]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* w_pal = reinterpret_cast<float*>(s_hdr + kPackTileBlocks * kMaxTex) + warp * 2 * p.pal_stride;   // [2][pal_stride]
   for (int i = tid; i < 352; i += blockDim.x)
     s_unorm[i] = i < 32 ? __fdiv_rn((float)i, 31.0f) : i < 96 ? __fdiv_rn((float)(i - 32), 63.0f)
                                                             : __fdiv_rn((float)(i - 96), 255.0f);
   if (tid < 32) s_unorm[352 + tid] = bc4_weight(tid);
 #if NTBC_CHECKS
-  NTBC_CHECK((uint32_t)(reinterpret_cast<uint8_t*>(s_hdr + kPackTileBlocks * kMaxTex) - reinterpret_cast<uint8_t*>(psm)) <=
+  NTBC_CHECK((uint32_t)(reinterpret_cast<uint8_t*>(w_pal + 2 * p.pal_stride) - reinterpret_cast<uint8_t*>(psm)) <=
              dyn_smem_bytes());
   for (int i = 384 + tid; i < 384 + kPackStages * stage_floats; i += blockDim.x)
     reinterpret_cast<uint32_t*>(psm)[i] = 0x7FC17FC1u;   // poison the staging buffers
@@ -633,7 +639,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
         bool swapped;
         const uint32_t hdr = quant_bc1_hdr(ep6, swapped);
         s_hdr[b * kMaxTex + k] = hdr;
-        if (NTBC_PACK_PAL) {
+        if (NTBC_PACK_PAL == 1) {
           const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
           const float e0[3] = {s_unorm[c0 >> 11], s_unorm[32 + ((c0 >> 5) & 63)], s_unorm[c0 & 31]};
           const float e1[3] = {s_unorm[c1 >> 11], s_unorm[32 + ((c1 >> 5) & 63)], s_unorm[c1 & 31]};
@@ -643,7 +649,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
         const float ep2[2] = {e[0], e[1]};
         const uint32_t hdr = quant_bc4_hdr(ep2);
         s_hdr[b * kMaxTex + k] = hdr;
-        if (NTBC_PACK_PAL) {
+        if (NTBC_PACK_PAL == 1) {
           const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
           bc4_palette_tab(s_unorm[96 + E0], s_unorm[96 + E1], E0 > E1, s_unorm + 352, dst);
         }
@@ -659,13 +665,31 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
       const bool single = p.vec16 ? (lane == 0 && wb + 1 >= nb) : ((lane & 15) == 0 && valid);
       const size_t oidx = (size_t)row * p.BW + bx0 + wb + (p.vec16 ? 0 : h);   // texture-independent word index
       NTBC_CHECK(!(pair || single) || (bx0 + wb + (pair ? 1 : p.vec16 ? 0 : h) < p.BW && row < p.rows));
+      if (NTBC_PACK_PAL == 2) {   // the two blocks' palettes, one (block, texture) per lane
+        __syncwarp();             // the previous pair's readers are done
+        if (lane < 2 * NT) {
+          const int hh = lane >= NT, k = lane - hh * NT, bb = min(wb + hh, nb - 1);
+          const uint32_t hdr = s_hdr[bb * kMaxTex + k];
+          float* dst = w_pal + hh * p.pal_stride + p.pal_off[k];
+          if (p.fmt[k] == kFmtBC1) {
+            const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
+            const float e0[3] = {s_unorm[c0 >> 11], s_unorm[32 + ((c0 >> 5) & 63)], s_unorm[c0 & 31]};
+            const float e1[3] = {s_unorm[c1 >> 11], s_unorm[32 + ((c1 >> 5) & 63)], s_unorm[c1 & 31]};
+            bc1_palette_pairs(e0, e1, dst);
+          } else {
+            const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
+            bc4_palette_tab(s_unorm[96 + E0], s_unorm[96 + E1], E0 > E1, s_unorm + 352, dst);
+          }
+        }
+        __syncwarp();
+      }
 #pragma unroll
       for (int k = 0; k < NT; k++) {
         const uint32_t hdr = s_hdr[b * kMaxTex + k];
         const int co = p.col_off[k];
         uint64_t idx[2];
         int shift;
-        const float* P = s_pal + b * p.pal_stride + p.pal_off[k];
+        const float* P = NTBC_PACK_PAL == 2 ? w_pal + h * p.pal_stride + p.pal_off[k] : s_pal + b * p.pal_stride + p.pal_off[k];
         if (NTBC_PACK_PAL && p.fmt[k] == kFmtBC1) {
           const float cc[3] = {c[co], c[co + 1], c[co + 2]};
           pack_bc1_indices2(bc1_code_pairs(cc, reinterpret_cast<const float2*>(P), (hdr & 0xFFFFu) == (hdr >> 16)), lane, idx);

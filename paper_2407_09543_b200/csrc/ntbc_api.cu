@@ -385,6 +385,11 @@ ntbc_status prepare_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream
   p.vec16 = (p.BW % 2) == 0;
   for (int k = 0; k < a.n_tex; k++)
     if ((uintptr_t)p.out[k] & 15) p.vec16 = 0;
+  p.n_bc1 = p.n_bc4 = 0;
+  for (int k = 0; k < a.n_tex; k++) {
+    if (a.fmt[k] == NTBC_BC1) p.tex_bc1[p.n_bc1++] = k;
+    else p.tex_bc4[p.n_bc4++] = k;
+  }
   return NTBC_OK;
 }
 

@@ -22,6 +22,10 @@ namespace ntbc {
 #ifndef NTBC_CHECKS
 #define NTBC_CHECKS 0
 #endif
+#ifndef NTBC_WARP_POLL
+#define NTBC_WARP_POLL 0   // 1: after a layer's MMAs every warp's lane 0 waits on the MMA mbarrier instead of one
+                           // thread + a 128-thread barrier (A/B r02g: 2.242 vs 2.201 ms, slower)
+#endif
 #if NTBC_CHECKS
 #define NTBC_CHECK(c)                                                                                  \
   do {                                                                                                 \
@@ -88,6 +92,8 @@ struct FusedParams {
   uint32_t tpal_off;            // byte offset of the colour tile's palettes inside a work group's region
   int vec16;                    // every out pointer 16-B aligned and BW even: a warp's two adjacent blocks'
                                 // words leave as one 16-byte store (else one 8-byte store per block)
+  int n_bc1, n_bc4;             // the texture indices of each format, in head order
+  int tex_bc1[kMaxTex], tex_bc4[kMaxTex];
 };
 
 // One fused launch: CTAs [0, split) run model m[0], CTAs [split, grid) run m[1] (the conservative pair,
@@ -335,8 +341,13 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
         issue_layer(tm, a_base, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
         mma_commit(bar_mma);
       }
+#if NTBC_WARP_POLL
+      if (lane == 0) mbar_wait(bar_mma, phase);     // one lane per warp polls: no 128-thread rendezvous
+      __syncwarp();
+#else
       if (r == issuer) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
       named_bar_sync(bar_id, 128);
+#endif
       phase ^= 1u;
       tc_fence_after();
       if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10), 16 columns at a time
@@ -464,12 +475,18 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
         // 16-byte store when p.vec16, else lanes 0 and 16 write one 8-byte word each
         const bool pair = p.vec16 && lane == 0 && b + 1 < nvalid;
         const bool single = p.vec16 ? (lane == 0 && b + 1 >= nvalid && b < nvalid) : ((lane & 15) == 0 && b < nvalid);
-        for (int k = 0; k < p.n_tex; k++) {
-          const int co = p.col_off[k];
-          const uint32_t hdr = hdrs[k * 128 + b];
-          uint64_t idx[2];
-          int shift;
-          if (NAIVE) {  // naive approach: nearest palette weight to the predicted weight
+        // the words of texture k: header | index field << SHIFT, both blocks of the warp (see above)
+        auto store = [&](int k, uint32_t hdr, const uint64_t* idx, int shift) {
+          uint64_t* dst = p.out[k] + out_row + bx;
+          NTBC_CHECK(!(pair || single) || (bx + (pair ? 1 : 0) < p.BW && by < p.row_end && b < kUnitBlocks));
+          if (pair) st_words2(dst, (uint64_t)hdr | (idx[0] << shift), (uint64_t)hdrs[k * 128 + b + 1] | (idx[1] << shift));
+          else if (single) *dst = (uint64_t)hdr | ((lane < 16 ? idx[0] : idx[1]) << shift);
+        };
+        if (NAIVE) {
+          for (int k = 0; k < p.n_tex; k++) {  // naive approach: nearest palette weight to the predicted weight
+            const int co = p.col_off[k];
+            const uint32_t hdr = hdrs[k * 128 + b];
+            uint64_t idx[2];
             const float w = stage[co * 128 + r];
             if (p.fmt[k] == kFmtBC1) {
               const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
@@ -477,30 +494,37 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
               if (swp[k * 128 + b]) n = 3u - n;                  // weights follow the predicted endpoint order
               const uint32_t code = c0 == c1 ? 0u : (0x1320u >> (4 * n)) & 3u;   // linear n -> code [0,2,3,1]
               pack_bc1_indices2(code, lane, idx);
-              shift = 32;
+              store(k, hdr, idx, 32);
             } else {
               const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
               const uint32_t n = naive_bc4_index(w, E0 > E1, unorm + 352);
               const uint32_t map = E0 > E1 ? 0x17654320u : 0x71543206u;
               pack_bc4_indices2((map >> (4 * n)) & 7u, lane, idx);
-              shift = 16;
+              store(k, hdr, idx, 16);
             }
-          } else if (p.fmt[k] == kFmtBC1) {  // the block's palette (precomputed at the tile start)
+          }
+        } else {
+          // BC1 textures, then BC4 textures (launch-uniform lists): no format branch per texture and
+          // constant field shifts; the block's palettes were built at the tile start
+          for (int t = 0; t < p.n_bc1; t++) {
+            const int k = p.tex_bc1[t], co = p.col_off[k];
+            const uint32_t hdr = hdrs[k * 128 + b];
             const float2* P = reinterpret_cast<const float2*>(tpal + (r >> 4) * p.pal_stride + p.pal_off[k]);
             const float c[3] = {stage[co * 128 + r], stage[(co + 1) * 128 + r], stage[(co + 2) * 128 + r]};
+            uint64_t idx[2];
             pack_bc1_indices2(bc1_code_pairs(c, P, (hdr & 0xFFFFu) == (hdr >> 16)), lane, idx);
-            shift = 32;
-          } else {
+            store(k, hdr, idx, 32);
+          }
+          for (int t = 0; t < p.n_bc4; t++) {
+            const int k = p.tex_bc4[t], co = p.col_off[k];
+            const uint32_t hdr = hdrs[k * 128 + b];
             const float4* P = reinterpret_cast<const float4*>(tpal + (r >> 4) * p.pal_stride + p.pal_off[k]);
             const float4 q0 = P[0], q1 = P[1];
             const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            uint64_t idx[2];
             pack_bc4_indices2(bc4_code(stage[co * 128 + r], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu)), lane, idx);
-            shift = 16;
+            store(k, hdr, idx, 16);
           }
-          uint64_t* dst = p.out[k] + out_row + bx;
-          NTBC_CHECK(!(pair || single) || (bx + (pair ? 1 : 0) < p.BW && by < p.row_end && b < kUnitBlocks));
-          if (pair) st_words2(dst, (uint64_t)hdr | (idx[0] << shift), (uint64_t)hdrs[k * 128 + b + 1] | (idx[1] << shift));
-          else if (single) *dst = (uint64_t)hdr | ((lane < 16 ? idx[0] : idx[1]) << shift);
         }
       }
     }
@@ -605,8 +629,9 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
                                                             : __fdiv_rn((float)(i - 96), 255.0f);
   if (tid < 32) s_unorm[352 + tid] = bc4_weight(tid);
 #if NTBC_CHECKS
-  NTBC_CHECK((uint32_t)(reinterpret_cast<uint8_t*>(w_pal + 2 * p.pal_stride) - reinterpret_cast<uint8_t*>(psm)) <=
-             dyn_smem_bytes());
+  NTBC_CHECK((uint32_t)(reinterpret_cast<uint8_t*>(NTBC_PACK_PAL == 2 ? w_pal + 2 * p.pal_stride
+                                                                     : reinterpret_cast<float*>(s_hdr + kPackTileBlocks * kMaxTex)) -
+                        reinterpret_cast<uint8_t*>(psm)) <= dyn_smem_bytes());
   for (int i = 384 + tid; i < 384 + kPackStages * stage_floats; i += blockDim.x)
     reinterpret_cast<uint32_t*>(psm)[i] = 0x7FC17FC1u;   // poison the staging buffers
   __syncthreads();
@@ -683,39 +708,43 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
         }
         __syncwarp();
       }
+      // the words of texture k: header | index field << SHIFT (lane 0: both blocks, one 16-byte store)
+      auto store = [&](int k, uint32_t hdr, const uint64_t* idx, int shift) {
+        if (pair) st_words2(p.out[k] + oidx, (uint64_t)hdr | (idx[0] << shift),
+                            (uint64_t)s_hdr[(b + 1) * kMaxTex + k] | (idx[1] << shift));
+        else if (single) p.out[k][oidx] = (uint64_t)hdr | ((lane < 16 ? idx[0] : idx[1]) << shift);
+      };
 #pragma unroll
       for (int k = 0; k < NT; k++) {
         const uint32_t hdr = s_hdr[b * kMaxTex + k];
         const int co = p.col_off[k];
         uint64_t idx[2];
-        int shift;
         const float* P = NTBC_PACK_PAL == 2 ? w_pal + h * p.pal_stride + p.pal_off[k] : s_pal + b * p.pal_stride + p.pal_off[k];
+        // texture loop unrolled over NT: format, offsets and output pointer are parameter-bank immediates
+        // (measured faster than BC1-then-BC4 runtime loops over index lists, r02i: 0.410 vs 0.461 ms)
         if (NTBC_PACK_PAL && p.fmt[k] == kFmtBC1) {
           const float cc[3] = {c[co], c[co + 1], c[co + 2]};
           pack_bc1_indices2(bc1_code_pairs(cc, reinterpret_cast<const float2*>(P), (hdr & 0xFFFFu) == (hdr >> 16)), lane, idx);
-          shift = 32;
+          store(k, hdr, idx, 32);
         } else if (NTBC_PACK_PAL) {
           const float4 q0 = reinterpret_cast<const float4*>(P)[0], q1 = reinterpret_cast<const float4*>(P)[1];
           const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
           pack_bc4_indices2(bc4_code(c[co], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu)), lane, idx);
-          shift = 16;
+          store(k, hdr, idx, 16);
         } else if (p.fmt[k] == kFmtBC1) {
           const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
           const float e0[3] = {s_unorm[c0 >> 11], s_unorm[32 + ((c0 >> 5) & 63)], s_unorm[c0 & 31]};
           const float e1[3] = {s_unorm[c1 >> 11], s_unorm[32 + ((c1 >> 5) & 63)], s_unorm[c1 & 31]};
           const float cc[3] = {c[co], c[co + 1], c[co + 2]};
           pack_bc1_indices2(bc1_code(cc, e0, e1, c0 == c1), lane, idx);
-          shift = 32;
+          store(k, hdr, idx, 32);
         } else {
           const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
           float pl[8];
           bc4_palette_tab(s_unorm[96 + E0], s_unorm[96 + E1], E0 > E1, s_unorm + 352, pl);
           pack_bc4_indices2(bc4_code(c[co], pl, E0 > E1), lane, idx);
-          shift = 16;
+          store(k, hdr, idx, 16);
         }
-        if (pair) st_words2(p.out[k] + oidx, (uint64_t)hdr | (idx[0] << shift),
-                            (uint64_t)s_hdr[(b + 1) * kMaxTex + k] | (idx[1] << shift));
-        else if (single) p.out[k][oidx] = (uint64_t)hdr | ((lane < 16 ? idx[0] : idx[1]) << shift);
       }
     }
   }

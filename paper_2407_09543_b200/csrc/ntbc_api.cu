@@ -293,9 +293,14 @@ ntbc_status launch_fused_t(const FusedLaunch& L, size_t smem, int grid, cudaStre
   return NTBC_OK;
 }
 
-size_t fused_smem(const FusedParams& p, int nwg) {
+// slots per work group of the fused kernel: 2 when the ping-pong variant runs (NTBC_PINGPONG, H = 64, 4 groups)
+int fused_slots(int hidden, int nwg, bool dump) { return (NTBC_PINGPONG && hidden == 64 && nwg == 4 && !dump) ? 2 : 1; }
+// per work group: SL A operands / staging buffers, the unit's BC word headers (+ naive swap flags), the
+// palettes of the SL tiles in flight (8 blocks each)
+uint32_t pal_bytes_of(const FusedParams& p, int sl) { return p.tpal_off + (uint32_t)(8 * sl * p.pal_stride * sizeof(float)); }
+size_t fused_smem(const FusedParams& p, int nwg, int sl = 1) {
   return (size_t)p.net[0].img_bytes + p.net[1].img_bytes + kOnesBytes + kUnormBytes +
-         (size_t)nwg * (p.a_bytes + p.pal_bytes) + 8 * (nwg + 1) + 16 + 4 * 8;
+         (size_t)nwg * (sl * p.a_bytes + pal_bytes_of(p, sl)) + 8 * (sl * nwg + 1) + 16 + 4 * 8;
 }
 
 ntbc_status launch_fused_locked(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream_t st);
@@ -405,16 +410,24 @@ ntbc_status launch_prepared(FusedParams* ps, int n, int hidden, bool dump, cudaS
   const size_t cap = 227 * 1024;
   int units = 0;
   for (int i = 0; i < n; i++) units += ps[i].n_units;
-  auto smem_of = [&](int w) { size_t m = 0; for (int i = 0; i < n; i++) m = std::max(m, fused_smem(ps[i], w)); return m; };
+  auto smem_of = [&](int w) {
+    size_t m = 0;
+    for (int i = 0; i < n; i++) m = std::max(m, fused_smem(ps[i], w, fused_slots(hidden, w, dump)));
+    return m;
+  };
   int nwg = 2;
   for (int w : {8, 4, 3})
-    if ((w != 8 || units >= 2 * 8 * sms) && smem_of(w) <= cap) { nwg = w; break; }
+    if ((w != 8 || units >= 2 * 8 * sms) && (w != 8 || !NTBC_PINGPONG || hidden != 64 || dump) && smem_of(w) <= cap) {
+      nwg = w;
+      break;
+    }
   if (const char* e = getenv("NTBC_NWG")) {  // measurement override (bench sweeps); clamped to what fits
     const int want = atoi(e);
     if ((want >= 2 && want <= 4 || want == 8) && smem_of(want) <= cap) nwg = want;
   }
   const size_t smem = smem_of(nwg);
   if (smem > cap) return fail(NTBC_EINVAL, "model needs %zu B of shared memory (> %zu)", smem, cap);
+  for (int i = 0; i < n; i++) ps[i].pal_bytes = pal_bytes_of(ps[i], fused_slots(hidden, nwg, dump));
   FusedLaunch L{};
   L.m[0] = ps[0];
   L.m[1] = n > 1 ? ps[1] : ps[0];

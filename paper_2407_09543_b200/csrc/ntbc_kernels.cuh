@@ -22,6 +22,12 @@ namespace ntbc {
 #ifndef NTBC_CHECKS
 #define NTBC_CHECKS 0
 #endif
+#ifndef NTBC_PINGPONG
+#define NTBC_PINGPONG 0    // 1: H = 64 models run 4 work groups of two colour tiles each, ping-ponged: each slot's
+                           // MMAs overlap the other slot's epilogue (correct -- 28 parity tests incl. the
+                           // full-size digests -- but slower, A/B r02j: 2.575 vs 2.201 ms: 16 warps per SM
+                           // hide less latency than 32)
+#endif
 #ifndef NTBC_WARP_POLL
 #define NTBC_WARP_POLL 0   // 1: after a layer's MMAs every warp's lane 0 waits on the MMA mbarrier instead of one
                            // thread + a 128-thread barrier (A/B r02g: 2.242 vs 2.201 ms, slower)
@@ -256,27 +262,31 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   const FusedParams& p = L.m[sel];
   const int cta = (int)blockIdx.x - (sel ? L.split : 0), ncta = sel ? (int)gridDim.x - L.split : L.split;
   const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5, lane = tid & 31;
+  // PP: two colour tiles per work group in flight (slots 0 / 1: A operand, TMEM accumulator, mbarrier), the
+  // MMAs of one slot overlapping the epilogue of the other (NTBC_PINGPONG, 4 work groups, H = 64)
+  constexpr bool PP = NTBC_PINGPONG && NWG == 4 && H == 64 && !DUMP;
+  constexpr int SL = PP ? 2 : 1;
 
   // ---- carve shared memory
   uint8_t* img_e = smem;                                          // endpoint net operand image
   uint8_t* img_c = smem + p.net[0].img_bytes;                     // colour net operand image
   uint8_t* ones = img_c + p.net[1].img_bytes;                     // [8][16] K-major, column 0 = 1.0
   float* unorm = reinterpret_cast<float*>(ones + kOnesBytes);           // q/31 [32], q/63 [64], q/255 [256], BC4 weights
-  uint8_t* wg_base = ones + kOnesBytes + kUnormBytes + wg * (p.a_bytes + p.pal_bytes);
+  uint8_t* wg_base = ones + kOnesBytes + kUnormBytes + wg * (SL * p.a_bytes + p.pal_bytes);
   uint8_t* A = wg_base;                                           // [128][H] K-major fp16 / fp32 staging
   float* stage = reinterpret_cast<float*>(A);                     // [ch][128] fp32 (after the last MMA)
-  uint32_t* hdrs = reinterpret_cast<uint32_t*>(wg_base + p.a_bytes);  // [tex][128 blocks] BC word low bits
+  uint32_t* hdrs = reinterpret_cast<uint32_t*>(wg_base + SL * p.a_bytes);  // [tex][128 blocks] BC word low bits
   uint8_t* swp = reinterpret_cast<uint8_t*>(hdrs + p.n_tex * 128);   // [tex][128 blocks] BC1 endpoint swap (naive)
-  float* tpal = reinterpret_cast<float*>(wg_base + p.a_bytes + p.tpal_off);   // [8 blocks][pal_stride] colour tile palettes
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ones + kOnesBytes + kUnormBytes + NWG * (p.a_bytes + p.pal_bytes));
-  uint64_t* bar_mma = bars + wg;                                  // this work group's MMA completion
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG + 1);
+  float* tpal = reinterpret_cast<float*>(wg_base + SL * p.a_bytes + p.tpal_off);   // [8 SL blocks][pal_stride] tile palettes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ones + kOnesBytes + kUnormBytes + NWG * (SL * p.a_bytes + p.pal_bytes));
+  uint64_t* bar_mma = bars + SL * wg;                             // this work group's MMA completion (per slot)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + SL * NWG + 1);
   int* next_slot = reinterpret_cast<int*>(tmem_slot + 1) + wg;    // dynamic scheduling: this group's next unit
 
 #if NTBC_CHECKS
   NTBC_CHECK((uint32_t)(reinterpret_cast<uint8_t*>(next_slot + NWG - wg) - smem) <= dyn_smem_bytes());
   NTBC_CHECK(p.a_bytes >= 128u * H * 2u && p.tpal_off >= (uint32_t)p.n_tex * 128u * 4u &&
-             p.pal_bytes >= p.tpal_off + 8u * p.pal_stride * 4u);
+             p.pal_bytes >= p.tpal_off + 8u * SL * p.pal_stride * 4u);
   for (uint32_t i = tid; i < (uint32_t)(reinterpret_cast<uint8_t*>(bars) - smem) / 4; i += NWG * 128)
     reinterpret_cast<uint32_t*>(smem)[i] = 0x7FC17FC1u;   // poison: fp32 and fp16 NaN
   fence_async_smem();
@@ -284,36 +294,39 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
 #endif
   // ---- the shared-memory prefix (operand images of both nets, ones tile, UNORM tables), prebuilt in global
   //      memory by the prep kernel: one bulk asynchronous copy (TMA engine) per 32 KB, completing on bar_img
-  uint64_t* bar_img = bars + NWG;
+  uint64_t* bar_img = bars + SL * NWG;
   if (tid == 0) {
-    for (int g = 0; g <= NWG; g++) mbar_init(bars + g, 1);
+    for (int g = 0; g <= SL * NWG; g++) mbar_init(bars + g, 1);
     fence_mbar_init();
     const uint32_t total = prefix_bytes(p.net);
     mbar_arrive_expect_tx(bar_img, total);
     for (uint32_t o = 0; o < total; o += 32768u)
       bulk_g2s(smem + o, p.prefix + o, min(32768u, total - o), bar_img);
   }
-  if (warp == 0) tmem_alloc(tmem_slot, NWG <= 2 ? 128 : NWG <= 4 ? 256 : 512);
+  constexpr uint32_t kTmemCols = SL * NWG <= 2 ? 128 : SL * NWG <= 4 ? 256 : 512;
+  if (warp == 0) tmem_alloc(tmem_slot, kTmemCols);
   __syncthreads();
   mbar_wait(bar_img, 0);   // the copy's writes are visible to this thread (generic reads of the tables) and to
                            // the tensor core (async-proxy reads of the operand images)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const uint32_t tm = tmem_base + (uint32_t)(wg * 64);                    // D columns of this group
-  NTBC_CHECK((tm & 0xFFFFu) + 64u <= (NWG <= 2 ? 128u : NWG <= 4 ? 256u : 512u));
+  const uint32_t tm = tmem_base + (uint32_t)(wg * 64 * SL);               // D columns of this group (slot 0)
+  NTBC_CHECK((tm & 0xFFFFu) + 64u * SL <= kTmemCols);
   const uint32_t tm_row = tm + ((uint32_t)(32 * (warp & 3)) << 16);       // this warp's TMEM lanes
   const uint32_t a_base = smem_u32(A), ones_base = smem_u32(ones);
   const uint32_t img_base[2] = {smem_u32(img_e), smem_u32(img_c)};
   const int bar_id = 1 + wg;
-  uint32_t phase = 0;
   // the thread that issues this group's MMAs: lane 0 of warp (wg mod 4) of the group, so the issuing
   // warps are spread over the four SM sub-partitions (warp w runs on SMSP w mod 4; measured: all eight
   // on SMSP 0 made each MMA cost ~275 issue cycles on the group's critical path, 2.25 -> 2.15 ms)
   const int issuer = 32 * (wg & 3);
 
-  // 16 grid features of row r (levels coarse->fine, 2 per level, R3) -> fp16 -> A columns 0..15
-  auto features = [&](int g, float pu, float pv, float* dump) {
+  uint32_t phase[SL];
+  for (int q = 0; q < SL; q++) phase[q] = 0;
+
+  // 16 grid features of row r (levels coarse->fine, 2 per level, R3) -> fp16 -> A columns 0..15 of slot sl
+  auto features = [&](int g, float pu, float pv, float* dump, int sl) {
     uint32_t hv[kMaxLevels];
 #pragma unroll
     for (int l = 0; l < kMaxLevels; l++) {
@@ -323,63 +336,78 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       const __half2 v = __floats2half2_rn(f0, f1);
       hv[l] = *reinterpret_cast<const uint32_t*>(&v);
     }
-    *reinterpret_cast<uint4*>(A + kmajor_offset(r, 0, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-    *reinterpret_cast<uint4*>(A + kmajor_offset(r, 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+    uint8_t* As = A + sl * p.a_bytes;
+    *reinterpret_cast<uint4*>(As + kmajor_offset(r, 0, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    *reinterpret_cast<uint4*>(As + kmajor_offset(r, 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
   };
 
-  // run the 4-layer MLP of net `n` on the A rows already written; leaves the output layer in TMEM
+  // layer l of net n on slot sl: the group's A rows are complete (barrier), one thread issues the MMAs
+  auto issue_l = [&](int n, int l, int sl) {
+    fence_async_smem();
+    tc_fence_before();
+    named_bar_sync(bar_id, 128);
+    if (r == issuer) {
+      tc_fence_after();
+      const int kin16 = l == 0 ? 16 : H;
+      const int N = l < 3 ? H : p.net[n].n_out16;
+      issue_layer(tm + sl * 64, a_base + sl * p.a_bytes, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
+      mma_commit(bar_mma + sl);
+    }
+  };
+  // wait for slot sl's MMAs.  One slot: one thread polls, the others park on bar.sync (measured faster than
+  // per-warp polling there); ping-pong: the MMAs ran during the other slot's epilogue, every warp polls once
+  auto wait_s = [&](int sl) {
+    if (PP || NTBC_WARP_POLL) {
+      if (lane == 0) mbar_wait(bar_mma + sl, phase[sl]);
+      __syncwarp();
+    } else {
+      if (r == issuer) mbar_wait(bar_mma + sl, phase[sl]);
+      named_bar_sync(bar_id, 128);
+    }
+    phase[sl] ^= 1u;
+    tc_fence_after();
+  };
+  // hidden layer epilogue of slot sl: selu -> fp16 -> next A operand row (R8-R10), 16 columns at a time
+  auto hidden_epi = [&](int sl) {
+    constexpr bool PF = NWG <= 4;   // prefetch the next chunk (16 more registers than NWG 8 has)
+    const uint32_t tr = tm_row + sl * 64;
+    uint8_t* As = A + sl * p.a_bytes;
+    uint32_t buf[2][16];
+    tmem_ld16p(tr, buf[0]);
+    tmem_wait_ld16(buf[0]);
+#pragma unroll
+    for (int c = 0; c < H / 16; c++) {
+      if (!PF && c > 0) {
+        tmem_ld16p(tr + c * 16, buf[c & 1]);
+        tmem_wait_ld16(buf[c & 1]);
+      }
+      if (PF && c + 1 < H / 16) tmem_ld16p(tr + (c + 1) * 16, buf[(c + 1) & 1]);
+      uint32_t hv[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
+      *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+      if (PF && c + 1 < H / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
+    }
+  };
+  // run the 4-layer MLP of net `n` on the A rows already written (slot 0); leaves the output layer in TMEM
   auto run_mlp = [&](int n) {
 #pragma unroll 1
     for (int l = 0; l < 4; l++) {
-      fence_async_smem();
-      tc_fence_before();
-      named_bar_sync(bar_id, 128);
-      if (r == issuer) {
-        tc_fence_after();
-        const int kin16 = l == 0 ? 16 : H;
-        const int N = l < 3 ? H : p.net[n].n_out16;
-        issue_layer(tm, a_base, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
-        mma_commit(bar_mma);
-      }
-#if NTBC_WARP_POLL
-      if (lane == 0) mbar_wait(bar_mma, phase);     // one lane per warp polls: no 128-thread rendezvous
-      __syncwarp();
-#else
-      if (r == issuer) mbar_wait(bar_mma, phase);   // one thread polls; the others park on bar.sync
-      named_bar_sync(bar_id, 128);
-#endif
-      phase ^= 1u;
-      tc_fence_after();
-      if (l < 3) {  // hidden layer epilogue: selu -> fp16 -> next A operand row (R8-R10), 16 columns at a time
-        constexpr bool PF = NWG <= 4;   // prefetch the next chunk (16 more registers than NWG 8 has)
-        uint32_t buf[2][16];
-        tmem_ld16p(tm_row, buf[0]);
-        tmem_wait_ld16(buf[0]);
-#pragma unroll
-        for (int c = 0; c < H / 16; c++) {
-          if (!PF && c > 0) {
-            tmem_ld16p(tm_row + c * 16, buf[c & 1]);
-            tmem_wait_ld16(buf[c & 1]);
-          }
-          if (PF && c + 1 < H / 16) tmem_ld16p(tm_row + (c + 1) * 16, buf[(c + 1) & 1]);
-          uint32_t hv[8];
-#pragma unroll
-          for (int j = 0; j < 8; j++)
-            hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
-          *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-          *reinterpret_cast<uint4*>(A + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
-          if (PF && c + 1 < H / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
-        }
-      }
+      issue_l(n, l, 0);
+      wait_s(0);
+      if (l < 3) hidden_epi(0);
     }
   };
-  // output layer epilogue: sigmoid of the output channels (pairs) -> fp32 staging [ch][128]
-  auto stage_outputs = [&](int n) {
+  // output layer epilogue of slot sl: sigmoid of the output channels (pairs) -> fp32 staging [ch][128] (in A)
+  auto stage_out = [&](int n, int sl) {
     const int no = p.net[n].n_out;
+    float* st = reinterpret_cast<float*>(A + sl * p.a_bytes);
 #pragma unroll 1
     for (int c16 = 0; c16 < no; c16 += 16) {
       uint32_t v[16];
-      tmem_ld16p(tm_row + c16, v);
+      tmem_ld16p(tm_row + sl * 64 + c16, v);
       tmem_wait_ld16(v);
 #pragma unroll
       for (int j = 0; j < 16; j += 2) {
@@ -388,12 +416,13 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           float s0, s1;
           sigmoid2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), s0, s1);
           NTBC_CHECK((uint32_t)((ch + 1) * 128 + r) * 4u < p.a_bytes);
-          stage[ch * 128 + r] = s0;
-          stage[(ch + 1) * 128 + r] = s1;
+          st[ch * 128 + r] = s0;
+          st[(ch + 1) * 128 + r] = s1;
         }
       }
     }
   };
+  auto stage_outputs = [&](int n) { stage_out(n, 0); };
 
 #pragma unroll 1
   for (int u = cta * NWG + wg; u < p.n_units;) {
@@ -411,7 +440,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       const float s = __fdiv_rn(__fadd_rn((float)min(bx0 + r, p.BW - 1), 0.5f), (float)p.BW);
       const float t = __fdiv_rn(__fadd_rn((float)by, 0.5f), (float)p.BH);
       float* fd = (DUMP && (p.debug_flags & 2) && r < nvalid) ? p.dump_ep + (out_row + bx0 + r) * 16 : nullptr;
-      features(0, s, t, fd);
+      features(0, s, t, fd, 0);
     }
     run_mlp(0);
     stage_outputs(0);
@@ -437,16 +466,78 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     }
 
     // ================= colour tiles: row r = texel (r & 15) of block 8j + (r >> 4)  (a1-a2, a4, a6-a8)
+    // index selection + packing of colour tile jt from slot sl's staged outputs (the block palettes at
+    // tpal[8 sl + r / 16] were built at the tile start)
+    auto pack_tile = [&](int jt, int sl) {
+      const int b = 8 * jt + (r >> 4);
+      const int bx = bx0 + b;
+      const float* st = reinterpret_cast<const float*>(A + sl * p.a_bytes);
+      const float* tp = tpal + (8 * sl + (r >> 4)) * p.pal_stride;
+      // lane 0 of each warp writes the words of the warp's two adjacent blocks (b, b + 1; bx even) as one
+      // 16-byte store when p.vec16, else lanes 0 and 16 write one 8-byte word each
+      const bool pair = p.vec16 && lane == 0 && b + 1 < nvalid;
+      const bool single = p.vec16 ? (lane == 0 && b + 1 >= nvalid && b < nvalid) : ((lane & 15) == 0 && b < nvalid);
+      // the words of texture k: header | index field << SHIFT, both blocks of the warp (see above)
+      auto store = [&](int k, uint32_t hdr, const uint64_t* idx, int shift) {
+        uint64_t* dst = p.out[k] + out_row + bx;
+        NTBC_CHECK(!(pair || single) || (bx + (pair ? 1 : 0) < p.BW && by < p.row_end && b < kUnitBlocks));
+        if (pair) st_words2(dst, (uint64_t)hdr | (idx[0] << shift), (uint64_t)hdrs[k * 128 + b + 1] | (idx[1] << shift));
+        else if (single) *dst = (uint64_t)hdr | ((lane < 16 ? idx[0] : idx[1]) << shift);
+      };
+      if (NAIVE) {
+        for (int k = 0; k < p.n_tex; k++) {  // naive approach: nearest palette weight to the predicted weight
+          const int co = p.col_off[k];
+          const uint32_t hdr = hdrs[k * 128 + b];
+          uint64_t idx[2];
+          const float w = st[co * 128 + r];
+          if (p.fmt[k] == kFmtBC1) {
+            const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
+            uint32_t n = naive_bc1_index(w);
+            if (swp[k * 128 + b]) n = 3u - n;                  // weights follow the predicted endpoint order
+            const uint32_t code = c0 == c1 ? 0u : (0x1320u >> (4 * n)) & 3u;   // linear n -> code [0,2,3,1]
+            pack_bc1_indices2(code, lane, idx);
+            store(k, hdr, idx, 32);
+          } else {
+            const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
+            const uint32_t n = naive_bc4_index(w, E0 > E1, unorm + 352);
+            const uint32_t map = E0 > E1 ? 0x17654320u : 0x71543206u;
+            pack_bc4_indices2((map >> (4 * n)) & 7u, lane, idx);
+            store(k, hdr, idx, 16);
+          }
+        }
+      } else {
+        // BC1 textures, then BC4 textures (launch-uniform lists): no format branch per texture and
+        // constant field shifts (A/B r02g: 2.201 vs 2.222 ms)
+        for (int t = 0; t < p.n_bc1; t++) {
+          const int k = p.tex_bc1[t], co = p.col_off[k];
+          const uint32_t hdr = hdrs[k * 128 + b];
+          const float2* P = reinterpret_cast<const float2*>(tp + p.pal_off[k]);
+          const float c[3] = {st[co * 128 + r], st[(co + 1) * 128 + r], st[(co + 2) * 128 + r]};
+          uint64_t idx[2];
+          pack_bc1_indices2(bc1_code_pairs(c, P, (hdr & 0xFFFFu) == (hdr >> 16)), lane, idx);
+          store(k, hdr, idx, 32);
+        }
+        for (int t = 0; t < p.n_bc4; t++) {
+          const int k = p.tex_bc4[t], co = p.col_off[k];
+          const uint32_t hdr = hdrs[k * 128 + b];
+          const float4* P = reinterpret_cast<const float4*>(tp + p.pal_off[k]);
+          const float4 q0 = P[0], q1 = P[1];
+          const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          uint64_t idx[2];
+          pack_bc4_indices2(bc4_code(st[co * 128 + r], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu)), lane, idx);
+          store(k, hdr, idx, 16);
+        }
+      }
+    };
 #pragma unroll 1
-    for (int j = 0; j < kUnitBlocks / 8 && 8 * j < nvalid; j++) {
-      const int b = 8 * j + (r >> 4), i = r & 15;
-      const int bx = bx0 + b, x = 4 * min(bx, p.BW - 1) + (i & 3), y = 4 * by + (i >> 2);
+    for (int j = 0; j < kUnitBlocks / 8 && 8 * j < nvalid; j += SL) {
+      const int ntile = (PP && 8 * (j + 1) < nvalid) ? 2 : 1;
       named_bar_sync(bar_id, 128);
-      if (!DUMP && !NAIVE && r < 8 * p.n_tex) {   // the tile's 8 x n_tex palettes, once per block (Eq.7/8, R18)
+      if (!DUMP && !NAIVE && r < 8 * ntile * p.n_tex) {   // the tiles' block palettes, once per block (Eq.7/8, R18)
         const int bl = r / p.n_tex, k = r - bl * p.n_tex;
         const uint32_t hdr = hdrs[k * 128 + 8 * j + bl];
         float* dst = tpal + bl * p.pal_stride + p.pal_off[k];
-        NTBC_CHECK(bl < 8 && k < p.n_tex && 8 * j + bl < kUnitBlocks);
+        NTBC_CHECK(bl < 8 * SL && k < p.n_tex && 8 * j + bl < kUnitBlocks);
         if (p.fmt[k] == kFmtBC1) {
           const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
           const float e0[3] = {unorm[c0 >> 11], unorm[32 + ((c0 >> 5) & 63)], unorm[c0 & 31]};
@@ -457,75 +548,40 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           bc4_palette_tab(unorm[96 + E0], unorm[96 + E1], E0 > E1, unorm + 352, dst);
         }
       }
-      {
+      for (int sl = 0; sl < ntile; sl++) {
+        const int b = 8 * (j + sl) + (r >> 4), i = r & 15;
+        const int bx = bx0 + b, x = 4 * min(bx, p.BW - 1) + (i & 3), y = 4 * by + (i >> 2);
         const float pu = __fdiv_rn(__fadd_rn((float)x, 0.5f), (float)p.W);
         const float pv = __fdiv_rn(__fadd_rn((float)y, 0.5f), (float)p.H);
         float* fd = (DUMP && (p.debug_flags & 2) && b < nvalid)
                         ? p.dump_col + (((size_t)(y - 4 * p.row_begin)) * p.W + x) * 16 : nullptr;
-        features(1, pu, pv, fd);
+        features(1, pu, pv, fd, sl);
       }
-      run_mlp(1);
-      stage_outputs(1);
+      if (!PP) {
+        run_mlp(1);
+        stage_outputs(1);
+      } else {   // ping-pong: slot 1's MMAs run during slot 0's epilogue and vice versa
+        for (int sl = 0; sl < ntile; sl++) issue_l(1, 0, sl);
+#pragma unroll 1
+        for (int l = 0; l < 4; l++)
+          for (int sl = 0; sl < ntile; sl++) {
+            wait_s(sl);
+            if (l < 3) {
+              hidden_epi(sl);
+              issue_l(1, l + 1, sl);
+            } else {
+              stage_out(1, sl);
+            }
+          }
+      }
       if (DUMP) {
+        const int b = 8 * j + (r >> 4), i = r & 15;
+        const int bx = bx0 + b, x = 4 * min(bx, p.BW - 1) + (i & 3), y = 4 * by + (i >> 2);
         if (b < nvalid && !(p.debug_flags & 2))
           for (int ch = 0; ch < p.net[1].n_out; ch++)
             p.dump_col[(((size_t)(y - 4 * p.row_begin)) * p.W + x) * p.net[1].n_out + ch] = stage[ch * 128 + r];
       } else {
-        // lane 0 of each warp writes the words of the warp's two adjacent blocks (b, b + 1; bx even) as one
-        // 16-byte store when p.vec16, else lanes 0 and 16 write one 8-byte word each
-        const bool pair = p.vec16 && lane == 0 && b + 1 < nvalid;
-        const bool single = p.vec16 ? (lane == 0 && b + 1 >= nvalid && b < nvalid) : ((lane & 15) == 0 && b < nvalid);
-        // the words of texture k: header | index field << SHIFT, both blocks of the warp (see above)
-        auto store = [&](int k, uint32_t hdr, const uint64_t* idx, int shift) {
-          uint64_t* dst = p.out[k] + out_row + bx;
-          NTBC_CHECK(!(pair || single) || (bx + (pair ? 1 : 0) < p.BW && by < p.row_end && b < kUnitBlocks));
-          if (pair) st_words2(dst, (uint64_t)hdr | (idx[0] << shift), (uint64_t)hdrs[k * 128 + b + 1] | (idx[1] << shift));
-          else if (single) *dst = (uint64_t)hdr | ((lane < 16 ? idx[0] : idx[1]) << shift);
-        };
-        if (NAIVE) {
-          for (int k = 0; k < p.n_tex; k++) {  // naive approach: nearest palette weight to the predicted weight
-            const int co = p.col_off[k];
-            const uint32_t hdr = hdrs[k * 128 + b];
-            uint64_t idx[2];
-            const float w = stage[co * 128 + r];
-            if (p.fmt[k] == kFmtBC1) {
-              const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
-              uint32_t n = naive_bc1_index(w);
-              if (swp[k * 128 + b]) n = 3u - n;                  // weights follow the predicted endpoint order
-              const uint32_t code = c0 == c1 ? 0u : (0x1320u >> (4 * n)) & 3u;   // linear n -> code [0,2,3,1]
-              pack_bc1_indices2(code, lane, idx);
-              store(k, hdr, idx, 32);
-            } else {
-              const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
-              const uint32_t n = naive_bc4_index(w, E0 > E1, unorm + 352);
-              const uint32_t map = E0 > E1 ? 0x17654320u : 0x71543206u;
-              pack_bc4_indices2((map >> (4 * n)) & 7u, lane, idx);
-              store(k, hdr, idx, 16);
-            }
-          }
-        } else {
-          // BC1 textures, then BC4 textures (launch-uniform lists): no format branch per texture and
-          // constant field shifts; the block's palettes were built at the tile start
-          for (int t = 0; t < p.n_bc1; t++) {
-            const int k = p.tex_bc1[t], co = p.col_off[k];
-            const uint32_t hdr = hdrs[k * 128 + b];
-            const float2* P = reinterpret_cast<const float2*>(tpal + (r >> 4) * p.pal_stride + p.pal_off[k]);
-            const float c[3] = {stage[co * 128 + r], stage[(co + 1) * 128 + r], stage[(co + 2) * 128 + r]};
-            uint64_t idx[2];
-            pack_bc1_indices2(bc1_code_pairs(c, P, (hdr & 0xFFFFu) == (hdr >> 16)), lane, idx);
-            store(k, hdr, idx, 32);
-          }
-          for (int t = 0; t < p.n_bc4; t++) {
-            const int k = p.tex_bc4[t], co = p.col_off[k];
-            const uint32_t hdr = hdrs[k * 128 + b];
-            const float4* P = reinterpret_cast<const float4*>(tpal + (r >> 4) * p.pal_stride + p.pal_off[k]);
-            const float4 q0 = P[0], q1 = P[1];
-            const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-            uint64_t idx[2];
-            pack_bc4_indices2(bc4_code(stage[co * 128 + r], pl, (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu)), lane, idx);
-            store(k, hdr, idx, 16);
-          }
-        }
+        for (int sl = 0; sl < ntile; sl++) pack_tile(j + sl, sl);
       }
     }
     if (!DUMP && p.progress) {  // publish the finished unit: group barrier, then one system-scope release
@@ -545,7 +601,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   // out pointers may be another GPU's memory mapped over NVLink (the fused peer gather, ntbc_peer_open)
   if (!DUMP && (lane & 15) == 0) __threadfence_system();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem_base, NWG <= 2 ? 128 : NWG <= 4 ? 256 : 512);
+  if (warp == 0) tmem_dealloc(tmem_base, kTmemCols);
 }
 
 // ---------------------------------------------------------------- kernel (2): standalone pack (a5-a8)

@@ -69,3 +69,41 @@ def test_gloo_gather_equals_single_process(world):
     assert np.array_equal(result["rows"].view(np.uint64), ref)
     for r, m in enumerate(result["mats"]):
         assert np.all(m == r)
+
+
+def _worker_batch(rank, world, port, n_mat, result):
+    """BASELINE config 5's host logic at world 2 on CPU: materials material_shards(n_mat, world)[rank] decoded
+    per rank (the oracle standing in for the GPU decode), gathered to rank 0 one material per rank per call
+    (bench.py's NCCL-gather fallback), assembled in global material order."""
+    import oracle
+    import synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        W, H = 32, 16
+        lo, hi = material_shards(n_mat, world)[rank]
+        batch = {}
+        for i, g in enumerate(range(lo, hi)):
+            words = oracle.Model(synth.model_blob(1, material=g)).decode_material(W, H)
+            got = gather_materials(torch.from_numpy(words.astype(np.int64).view(np.int64)), rank, world)
+            if rank == 0:
+                for r, t in enumerate(got):
+                    batch[material_shards(n_mat, world)[r][0] + i] = t.numpy().copy()
+        if rank == 0:
+            result["batch"] = [batch[g] for g in range(n_mat)]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_material_batch_equals_single_process():
+    import oracle
+    import synth
+    n_mat, world = 4, 2
+    mgr = mp.get_context("spawn").Manager()
+    result = mgr.dict()
+    mp.start_processes(_worker_batch, args=(world, _free_port(), n_mat, result), nprocs=world, join=True,
+                       start_method="spawn")
+    for g, words in enumerate(result["batch"]):
+        ref = oracle.Model(synth.model_blob(1, material=g)).decode_material(32, 16)
+        assert np.array_equal(words.view(np.uint64), ref), g

@@ -28,6 +28,11 @@ namespace ntbc {
                            // full-size digests -- but slower, A/B r02j: 2.575 vs 2.201 ms: 16 warps per SM
                            // hide less latency than 32)
 #endif
+#ifndef NTBC_TMEM_PF8
+#define NTBC_TMEM_PF8 0    // 1: hidden epilogue loads TMEM in 8-column chunks with the next chunk in flight (same
+                           // registers as the x16 loads; A/B r02l: 2.214 vs 2.197 ms, slower -- the TMEM load
+                           // latency is not what the warps wait for)
+#endif
 #ifndef NTBC_WARP_POLL
 #define NTBC_WARP_POLL 0   // 1: after a layer's MMAs every warp's lane 0 waits on the MMA mbarrier instead of one
                            // thread + a 128-thread barrier (A/B r02g: 2.242 vs 2.201 ms, slower)
@@ -220,6 +225,18 @@ __device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld8p(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld8(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t& a, uint32_t& b) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a), "+r"(b)::"memory");
@@ -372,6 +389,22 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     constexpr bool PF = NWG <= 4;   // prefetch the next chunk (16 more registers than NWG 8 has)
     const uint32_t tr = tm_row + sl * 64;
     uint8_t* As = A + sl * p.a_bytes;
+    if (NTBC_TMEM_PF8 && !PF) {     // 8-column chunks, the next chunk's load in flight during this chunk's selu
+      uint32_t b8[2][8];
+      tmem_ld8p(tr, b8[0]);
+      tmem_wait_ld8(b8[0]);
+#pragma unroll
+      for (int c = 0; c < H / 8; c++) {
+        if (c + 1 < H / 8) tmem_ld8p(tr + (c + 1) * 8, b8[(c + 1) & 1]);
+        uint32_t hv[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          hv[j] = selu2_h2(__uint_as_float(b8[c & 1][2 * j]), __uint_as_float(b8[c & 1][2 * j + 1]));
+        *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 8, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+        if (c + 1 < H / 8) tmem_wait_ld8(b8[(c + 1) & 1]);
+      }
+      return;
+    }
     uint32_t buf[2][16];
     tmem_ld16p(tr, buf[0]);
     tmem_wait_ld16(buf[0]);

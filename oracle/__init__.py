@@ -80,6 +80,7 @@ def lib():
             "o_exp_max_relerr": (C.c_double, [f32, f32, i32, i32]),
             "o_set_act_model": (None, [i32]),
             "o_get_act_model": (i32, []),
+            "o_set_operand_model": (None, [i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

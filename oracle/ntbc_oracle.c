@@ -410,17 +410,47 @@ void o_grid_encode(const o_model* m, int which, float p, float q, float* out) {
 /* MLP: fp16 operands at every layer input, selu hidden,       */
 /* sigmoid output                                                 */
 /* ------------------------------------------------------------------------- */
+/* Operand contract of every layer input.  0 = H, the paper's half precision (P:322,
+   P:331): a -> RN16(a), what the kernels compute.  1 = F ("fp32-faithful", a sensitivity study only, not
+   implemented on the GPU): activations stay binary32 and each MMA operand is the split hi = RN16(a),
+   lo = RN16(a - hi), the dot product running over [hi 0:16, lo 0:16, hi 16:32, lo 16:32, ...] with the
+   weights repeated. */
+static int g_operand_split = 0;
+void o_set_operand_model(int split) { g_operand_split = split; }
+
 void o_mlp_raw(int n_layers, const int* dims, const uint16_t* const* W, const uint16_t* const* b,
                const float* in, float* out) {
     float act[256];
-    uint16_t a16[256];
+    uint16_t a16[512], w2[512];
     for (int i = 0; i < dims[0]; i++) act[i] = in[i];
     for (int l = 0; l < n_layers; l++) {
         int K = dims[l], N = dims[l + 1];
-        for (int i = 0; i < K; i++) a16[i] = o_f32_to_f16(act[i]);
-        for (int j = 0; j < N; j++) {
-            float z = o_dot(o_f16_to_f32(b[l][j]), W[l] + j, N, a16, K);
-            act[j] = (l + 1 < n_layers) ? o_selu(z) : o_sigmoid(z);
+        if (!g_operand_split) {
+            for (int i = 0; i < K; i++) a16[i] = o_f32_to_f16(act[i]);
+            for (int j = 0; j < N; j++) {
+                float z = o_dot(o_f16_to_f32(b[l][j]), W[l] + j, N, a16, K);
+                act[j] = (l + 1 < n_layers) ? o_selu(z) : o_sigmoid(z);
+            }
+        } else {
+            int K2 = 0;
+            for (int k0 = 0; k0 < K; k0 += 16) {          /* interleaved 16-wide hi / lo chunks */
+                int k1 = k0 + 16 < K ? k0 + 16 : K;
+                for (int i = k0; i < k1; i++) a16[K2++] = o_f32_to_f16(act[i]);
+                for (int i = k0; i < k1; i++) {
+                    float hi = o_f16_to_f32(o_f32_to_f16(act[i]));
+                    a16[K2++] = o_f32_to_f16(act[i] - hi);
+                }
+            }
+            for (int j = 0; j < N; j++) {
+                int n2 = 0;
+                for (int k0 = 0; k0 < K; k0 += 16) {
+                    int k1 = k0 + 16 < K ? k0 + 16 : K;
+                    for (int rep = 0; rep < 2; rep++)
+                        for (int i = k0; i < k1; i++) w2[n2++] = W[l][(size_t)i * N + j];
+                }
+                float z = o_dot(o_f16_to_f32(b[l][j]), w2, 1, a16, K2);
+                act[j] = (l + 1 < n_layers) ? o_selu(z) : o_sigmoid(z);
+            }
         }
     }
     for (int j = 0; j < dims[n_layers]; j++) out[j] = act[j];

@@ -64,6 +64,9 @@ float o_fused_sum(const float* acc_in, const uint16_t* a, const uint16_t* b, int
 void o_grid_encode(const o_model* m, int which, float p, float q, float* out);
 /* ---- MLP: which 0 = endpoint net, 1 = colour net ---- */
 void o_mlp_forward(const o_model* m, int which, const float* in, float* out);
+/* operand contract: 0 = H (binary16 layer inputs, the paper's and the kernels'), 1 = F (fp32 activations,
+   hi/lo split operands; sensitivity study of DESIGN.md §5.1 only) */
+void o_set_operand_model(int split);
 /* raw MLP on caller-given fp16 params (for the torch pins) */
 void o_mlp_raw(int n_layers, const int* dims, const uint16_t* const* W, const uint16_t* const* b,
                const float* in, float* out);

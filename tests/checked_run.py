@@ -54,6 +54,21 @@ def main():
         for k in range(m.n_tex):
             got = u64(part[k])[1:1 + (r1 - r0) * (w // 4)].reshape(r1 - r0, w // 4)
             assert np.array_equal(got, ref[k]), ("shard", w, hh, k)
+    # seeded random models and shapes (tests/fuzz_cases.py), shards into 8-B-only aligned planes included
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from fuzz_cases import cases as fuzz_cases
+    for blob, w, hh, r0, r1, misalign in fuzz_cases(24, seed=77):
+        m = ntbc.Model(blob)
+        rows, bw = r1 - r0, w // 4
+        buf = torch.full((m.n_tex, rows * bw + 2), -1, dtype=torch.int64, device="cuda")
+        ntbc.decode_material([m], w, hh, row_begin=r0, row_end=r1,
+                             out_ptrs=[buf[k].data_ptr() + (8 if misalign else 0) for k in range(m.n_tex)])
+        ref = oracle.Model(blob).decode_material(w, hh, r0, r1)
+        off = 1 if misalign else 0
+        for k in range(m.n_tex):
+            got = u64(buf[k])[off:off + rows * bw].reshape(rows, bw)
+            assert np.array_equal(got, ref[k]), ("fuzz", w, hh, k)
+            h.update(got.tobytes())
     # conservative pair (one launch, CTAs partitioned by model)
     rgb = synth.serialize(synth.random_model(synth.ModelSpec([synth.BC1, synth.BC1], block_levels=4, texel_levels=5), 5))
     sc = synth.serialize(synth.random_model(synth.ModelSpec([synth.BC4] * 4, block_levels=4, texel_levels=5), 6))

@@ -66,25 +66,29 @@ def test_plain_dot_is_exact_sum_rounded_once():
 
 
 # ---------------------------------------------------------------- the measurement
-def _material_report(cfg, rows, dot=None, act=None):
+def _material_report(cfg, rows, dot=None, act=None, split=0):
     """Words + MLP outputs of `rows` of config `cfg` in the oracle mode (dot, act) vs the plain mode."""
     W, H, _ = synth.config_shape(cfg)
     om = oracle.Model(synth.model_blob(cfg))
     r0, r1 = rows
     saved = (oracle.get_dot_model(), int(L.o_get_act_model()))
     try:
+        L.o_set_operand_model(split)
         if dot is not None:
             oracle.set_dot_model(*dot)
         if act is not None:
             oracle.set_act_model(act)
         w = om.decode_material(W, H, r0, r1)
         ep, col = om.mlp_outputs(W, H, r0, r1)
+        oracle.set_dot_model(*saved[0])
+        oracle.set_act_model(saved[1])
+        with oracle.plain_definitions():
+            pw = om.decode_material(W, H, r0, r1)
+            pep, pcol = om.mlp_outputs(W, H, r0, r1)
     finally:
         oracle.set_dot_model(*saved[0])
         oracle.set_act_model(saved[1])
-    with oracle.plain_definitions():
-        pw = om.decode_material(W, H, r0, r1)
-        pep, pcol = om.mlp_outputs(W, H, r0, r1)
+        L.o_set_operand_model(0)
     rep = compare_words(om.fmts, w, pw, pep, pcol)
     rep["endpoint_floats"] = float_stats(ep, pep)
     rep["colour_floats"] = float_stats(col, pcol)
@@ -136,6 +140,23 @@ def test_pinned_arithmetic_within_the_half_precision_floor(reports, cfg):
     for key in ("mismatched", "unexcused"):
         floor = max(o[key] for o in others)
         assert pin[key] <= 2 * floor + 4, (key, pin[key], floor)
+
+
+def test_contract_f_pinned_arithmetic_meets_the_literal_rule():
+    """With binary32 activations (contract F of SURVEY §8.c.3: each MMA operand the split hi = RN16(a),
+    lo = RN16(a - hi)) the pinned arithmetic -- R9 v4's exponential, R10's tensor-core summation order --
+    meets north_star's rule LITERALLY against the plain definitions of the same contract: floats within
+    1e-3 relative, zero unexcused words, excused words under 1e-4 of the blocks.  So the floor measured under
+    the paper's half precision (contract H, test_pinned_arithmetic_within_the_half_precision_floor) is the
+    contract's, not the pinned arithmetic's."""
+    rep = _material_report(2, (0, 32), split=1)
+    print(f"\nC2 rows 0-31, contract F, pinned vs plain: {rep['mismatched']} of {rep['words']} words differ "
+          f"({rep['excused']} excused, {rep['unexcused']} unexcused); max rel endpoint "
+          f"{rep['endpoint_floats']['max_rel']:.2e} colour {rep['colour_floats']['max_rel']:.2e}")
+    assert rep["endpoint_floats"]["max_rel"] <= 1e-3 and rep["colour_floats"]["max_rel"] <= 1e-3
+    assert rep["endpoint_floats"]["zero_violations"] == 0 and rep["colour_floats"]["zero_violations"] == 0
+    assert rep["unexcused"] == 0
+    assert rep["excused"] < 1e-4 * rep["blocks"]
 
 
 def test_mismatch_classes_account_for_every_word(reports):

@@ -221,6 +221,15 @@ ntbc_status ntbc_peer_close(void* device_ptr);
 /* Number of kernel launches the library issued since load (all entry points), for bench accounting. */
 uint64_t ntbc_launch_count(void);
 
+/* The arithmetic contract of the model's MLP operands.  0 = H (default):
+ * every layer input rounded to binary16, the paper's half-precision inference.
+ * 1 = F: activations stay binary32 and each tcgen05 operand is the split hi = RN16(a), lo = RN16(a - hi),
+ * multiplied by the same weights (2x the MMAs, half the work groups per SM) -- the contract under which the
+ * decode meets north_star's agreement rule against the plain definitions literally.  Both are bit-exact
+ * against the oracle's matching mode.  Applies to later decodes of the model (serialised with them).
+ * Errors: NTBC_EINVAL (NULL, contract not 0/1, F for a naive model). */
+ntbc_status ntbc_set_contract(ntbc_model m, int contract);
+
 /* Measurement hook (bench.py's roofline of the dominant kernel): while set, every fused-kernel launch
  * made by THIS host thread through ntbc_decode_material / ntbc_decode_material_host records
  * `start_event` right before and `end_event` right after it on the launch stream (cudaEvent_t as

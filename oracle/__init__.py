@@ -189,6 +189,24 @@ def set_act_model(plain: int):
     lib().o_set_act_model(int(plain))
 
 
+def set_operand_model(split: int):
+    """0 = contract H (binary16 layer inputs, the kernels' default); 1 = contract F (binary32 activations,
+    hi/lo split operands; the library's ntbc_set_contract(m, 1))."""
+    lib().o_set_operand_model(int(split))
+
+
+class contract_f:
+    """Context manager: the oracle computes contract F (its pinned or plain arithmetic as set otherwise)."""
+
+    def __enter__(self):
+        set_operand_model(1)
+        return self
+
+    def __exit__(self, *exc):
+        set_operand_model(0)
+        return False
+
+
 class plain_definitions:
     """Context manager: the oracle computes the PLAIN definitions (every dot product exact and rounded
     once, selu / sigmoid in float64 with libm, one rounding) instead of the pinned op sequences the

@@ -432,22 +432,22 @@ void o_mlp_raw(int n_layers, const int* dims, const uint16_t* const* W, const ui
                 act[j] = (l + 1 < n_layers) ? o_selu(z) : o_sigmoid(z);
             }
         } else {
+            /* interleaved hi / lo chunks of 16 entries (a partial chunk padded with zero operands, which
+               add no term to any sum), so that R10's chunks of 16 are exactly the tensor core's K = 16 MMAs */
             int K2 = 0;
-            for (int k0 = 0; k0 < K; k0 += 16) {          /* interleaved 16-wide hi / lo chunks */
-                int k1 = k0 + 16 < K ? k0 + 16 : K;
-                for (int i = k0; i < k1; i++) a16[K2++] = o_f32_to_f16(act[i]);
-                for (int i = k0; i < k1; i++) {
+            for (int k0 = 0; k0 < K; k0 += 16) {
+                for (int i = k0; i < k0 + 16; i++) a16[K2++] = i < K ? o_f32_to_f16(act[i]) : 0;
+                for (int i = k0; i < k0 + 16; i++) {
+                    if (i >= K) { a16[K2++] = 0; continue; }
                     float hi = o_f16_to_f32(o_f32_to_f16(act[i]));
                     a16[K2++] = o_f32_to_f16(act[i] - hi);
                 }
             }
             for (int j = 0; j < N; j++) {
                 int n2 = 0;
-                for (int k0 = 0; k0 < K; k0 += 16) {
-                    int k1 = k0 + 16 < K ? k0 + 16 : K;
+                for (int k0 = 0; k0 < K; k0 += 16)
                     for (int rep = 0; rep < 2; rep++)
-                        for (int i = k0; i < k1; i++) w2[n2++] = W[l][(size_t)i * N + j];
-                }
+                        for (int i = k0; i < k0 + 16; i++) w2[n2++] = i < K ? W[l][(size_t)i * N + j] : 0;
                 float z = o_dot(o_f16_to_f32(b[l][j]), w2, 1, a16, K2);
                 act[j] = (l + 1 < n_layers) ? o_selu(z) : o_sigmoid(z);
             }

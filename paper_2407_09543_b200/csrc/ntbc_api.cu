@@ -179,6 +179,7 @@ struct ntbc_model_s {
   // decodes of one model on different streams are ordered on the device by `last_done`, recorded after
   // each launch (they share the model's fp32 grid region, rewritten by every decode's dequant launch)
   std::recursive_mutex mu;
+  int contract = 0;            // MMA operand contract: 0 = H (binary16 activations), 1 = F
   cudaEvent_t last_done = nullptr;
   cudaStream_t last_stream = nullptr;
   uint8_t* d_blob = nullptr;   // weight slot: the blob, then at fg_base its grids dequantized to fp32
@@ -281,9 +282,10 @@ struct DevGuard {
   ~DevGuard() { int cur; cudaGetDevice(&cur); if (prev >= 0 && cur != prev) cudaSetDevice(prev); }
 };
 
-template <int H, int NWG, bool DUMP>
+template <int H, int NWG, bool DUMP, bool SPLIT = false>
 ntbc_status launch_fused_t(const FusedLaunch& L, size_t smem, int grid, cudaStream_t st) {
-  auto kern = L.m[0].naive ? fused_decode_kernel<H, NWG, DUMP, true> : fused_decode_kernel<H, NWG, DUMP, false>;
+  auto kern = SPLIT ? fused_decode_kernel<H, NWG, DUMP, false, true>
+                    : L.m[0].naive ? fused_decode_kernel<H, NWG, DUMP, true> : fused_decode_kernel<H, NWG, DUMP, false>;
   CUDA_TRY(allow_smem((const void*)kern, 227 * 1024));
   if (!DUMP && g_time_fused[0]) CUDA_TRY(cudaEventRecord(g_time_fused[0], st));
   kern<<<grid, NWG * 128, smem, st>>>(L);
@@ -374,7 +376,9 @@ ntbc_status prepare_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream
   p.units_per_row = (p.BW + kUnitBlocks - 1) / kUnitBlocks;
   p.n_units = p.units_per_row * (p.row_end - p.row_begin);
   const int maxo = a.dims[0][4] > a.dims[1][4] ? a.dims[0][4] : a.dims[1][4];
-  const uint32_t a_kmajor = 128u * a.hidden * 2u, a_stage = 128u * 4u * (uint32_t)((maxo + 1) & ~1);  // pairs
+  p.split = m->contract;
+  const uint32_t a_kmajor = 128u * a.hidden * 2u * (p.split ? 2u : 1u);   // F: hi and lo chunks
+  const uint32_t a_stage = 128u * 4u * (uint32_t)((maxo + 1) & ~1);      // fp32 staging [ch][128], pairs
   p.a_bytes = (uint32_t)((std::max(a_kmajor, a_stage) + 127) & ~127u);
   // per work group: BC word headers (+ BC1 swap flags, naive models) of the unit's 128 blocks, then the palettes of the
   // current colour tile's 8 blocks (BC1 12 floats, BC4 8 floats per texture; 16-B aligned records)
@@ -417,13 +421,14 @@ ntbc_status launch_prepared(FusedParams* ps, int n, int hidden, bool dump, cudaS
   };
   int nwg = 2;
   for (int w : {8, 4, 3})
-    if ((w != 8 || units >= 2 * 8 * sms) && (w != 8 || !NTBC_PINGPONG || hidden != 64 || dump) && smem_of(w) <= cap) {
+    if ((w != 8 || units >= 2 * 8 * sms) && (w != 8 || !NTBC_PINGPONG || hidden != 64 || dump) && (w != 8 || !ps[0].split) &&
+        smem_of(w) <= cap) {
       nwg = w;
       break;
     }
   if (const char* e = getenv("NTBC_NWG")) {  // measurement override (bench sweeps); clamped to what fits
     const int want = atoi(e);
-    if ((want >= 2 && want <= 4 || want == 8) && smem_of(want) <= cap) nwg = want;
+    if ((want >= 2 && want <= 4 || (want == 8 && !ps[0].split)) && smem_of(want) <= cap) nwg = want;
   }
   const size_t smem = smem_of(nwg);
   if (smem > cap) return fail(NTBC_EINVAL, "model needs %zu B of shared memory (> %zu)", smem, cap);
@@ -445,6 +450,18 @@ ntbc_status launch_prepared(FusedParams* ps, int n, int hidden, bool dump, cudaS
     if (const char* e = getenv("NTBC_PAIR_SPLIT")) split = atoi(e);   // measurement override
     L.split = std::max(1, std::min(grid - 1, split));
   }
+#define NTBC_DISPATCH_SPLIT(HH)                                                                  \
+  if (hidden == HH && ps[0].split) {                                                             \
+    if (nwg == 4) return dump ? launch_fused_t<HH, 4, true, true>(L, smem, grid, st)             \
+                              : launch_fused_t<HH, 4, false, true>(L, smem, grid, st);           \
+    if (nwg == 3) return dump ? launch_fused_t<HH, 3, true, true>(L, smem, grid, st)             \
+                              : launch_fused_t<HH, 3, false, true>(L, smem, grid, st);           \
+    return dump ? launch_fused_t<HH, 2, true, true>(L, smem, grid, st) : launch_fused_t<HH, 2, false, true>(L, smem, grid, st); \
+  }
+  NTBC_DISPATCH_SPLIT(16)
+  NTBC_DISPATCH_SPLIT(32)
+  NTBC_DISPATCH_SPLIT(64)
+#undef NTBC_DISPATCH_SPLIT
 #define NTBC_DISPATCH(HH)                                                                        \
   if (hidden == HH) {                                                                            \
     if (nwg == 8) return dump ? launch_fused_t<HH, 8, true>(L, smem, grid, st)                   \
@@ -682,6 +699,7 @@ ntbc_status ntbc_decode_material(const ntbc_model* models, int n_models, int wid
   }
   cudaStream_t cs = (cudaStream_t)stream;
   if (n_models == 1 || models[0]->arch.hidden != models[1]->arch.hidden || models[0]->arch.naive != models[1]->arch.naive ||
+      models[0]->contract != models[1]->contract ||
       (getenv("NTBC_PAIR_LAUNCHES") && atoi(getenv("NTBC_PAIR_LAUNCHES")))) {
     for (int i = 0; i < n_models; i++) {   // one fused launch per model
       DevGuard dg(models[i]->device);
@@ -1139,6 +1157,15 @@ ntbc_status ntbc_debug_mma(const void* A, const void* B, const float* C, float* 
 }
 
 uint64_t ntbc_launch_count(void) { return g_launches.load(); }
+
+ntbc_status ntbc_set_contract(ntbc_model m, int contract) {
+  if (!m) return fail(NTBC_EINVAL, "model is NULL");
+  if (contract != 0 && contract != 1) return fail(NTBC_EINVAL, "contract %d not in {0 (H), 1 (F)}", contract);
+  if (contract == 1 && m->arch.naive) return fail(NTBC_EINVAL, "contract F is not provided for the naive variant");
+  std::lock_guard<std::recursive_mutex> lk(m->mu);
+  m->contract = contract;
+  return NTBC_OK;
+}
 
 ntbc_status ntbc_debug_time_fused(void* start_event, void* end_event) {
   if ((start_event == nullptr) != (end_event == nullptr)) return fail(NTBC_EINVAL, "pass both events or neither");

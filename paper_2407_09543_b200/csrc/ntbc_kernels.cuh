@@ -103,6 +103,7 @@ struct FusedParams {
   uint32_t tpal_off;            // byte offset of the colour tile's palettes inside a work group's region
   int vec16;                    // every out pointer 16-B aligned and BW even: a warp's two adjacent blocks'
                                 // words leave as one 16-byte store (else one 8-byte store per block)
+  int split;                    // contract F (host side; the kernel's SPLIT template parameter follows it)
   int n_bc1, n_bc4;             // the texture indices of each format, in head order
   int tex_bc1[kMaxTex], tex_bc4[kMaxTex];
 };
@@ -255,14 +256,19 @@ __device__ __forceinline__ void tmem_wait_ld16(uint32_t* r) {
 // Issue one layer of the MLP for the 128 rows of a work group (called by ONE thread):
 // bias chunk first (A = ones tile, B = bias column; overwrites D), then the K/16 activation chunks
 // in increasing k (accumulate) -- the summation order pinned by R10.
+// SPLIT (contract F): A holds each 16-wide K chunk c of the activations as two physical chunks, hi at 2c and
+// lo at 2c + 1; both are multiplied by the same B chunk, hi first (the order the oracle's F mode pins).
+template <bool SPLIT = false>
 __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, int K_A, uint32_t ones_base,
                                             uint32_t b_base, int kin16, int N) {
   const int K_B = kin16 + 16;
   const uint32_t idesc = idesc_f16_f32(128, N);
   mma_f16(tmem_d, smem_desc(ones_base, 128, 0), smem_desc(b_base + (kin16 / 16) * 256, 128, K_B * 16), idesc, 0u);
-  for (int c = 0; c < kin16 / 16; c++)
-    mma_f16(tmem_d, smem_desc(a_base + c * 256, 128, K_A * 16), smem_desc(b_base + c * 256, 128, K_B * 16), idesc,
-            1u);
+  for (int c = 0; c < kin16 / 16; c++) {
+    const uint64_t bd = smem_desc(b_base + c * 256, 128, K_B * 16);
+    mma_f16(tmem_d, smem_desc(a_base + (SPLIT ? 2 * c : c) * 256, 128, K_A * 16), bd, idesc, 1u);
+    if (SPLIT) mma_f16(tmem_d, smem_desc(a_base + (2 * c + 1) * 256, 128, K_A * 16), bd, idesc, 1u);
+  }
 }
 
 // ---------------------------------------------------------------- kernel (1): fused decode
@@ -272,8 +278,9 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, in
 // (128 blocks) then up to 16 colour tiles (8 blocks = 128 texels).  More independent groups per SM
 // hide more of the dependent epilogue latency.  Units are claimed from a global
 // counter (dynamic scheduling) so they finish in row order (pipelined copy-back, ntbc_api.cu).
-template <int H, int NWG, bool DUMP, bool NAIVE>
+template <int H, int NWG, bool DUMP, bool NAIVE, bool SPLIT = false>
 __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid_constant__ FusedLaunch L) {
+  constexpr int KA = SPLIT ? 2 * H : H;   // K width (fp16 columns) of the A operand rows
   extern __shared__ __align__(1024) uint8_t smem[];
   const int sel = (int)blockIdx.x >= L.split;          // which model this CTA decodes
   const FusedParams& p = L.m[sel];
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
   const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5, lane = tid & 31;
   // PP: two colour tiles per work group in flight (slots 0 / 1: A operand, TMEM accumulator, mbarrier), the
   // MMAs of one slot overlapping the epilogue of the other (NTBC_PINGPONG, 4 work groups, H = 64)
-  constexpr bool PP = NTBC_PINGPONG && NWG == 4 && H == 64 && !DUMP;
+  constexpr bool PP = NTBC_PINGPONG && NWG == 4 && H == 64 && !DUMP && !SPLIT;
   constexpr int SL = PP ? 2 : 1;
 
   // ---- carve shared memory
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
 
 #if NTBC_CHECKS
   NTBC_CHECK((uint32_t)(reinterpret_cast<uint8_t*>(next_slot + NWG - wg) - smem) <= dyn_smem_bytes());
-  NTBC_CHECK(p.a_bytes >= 128u * H * 2u && p.tpal_off >= (uint32_t)p.n_tex * 128u * 4u &&
+  NTBC_CHECK(p.a_bytes >= 128u * KA * 2u && p.tpal_off >= (uint32_t)p.n_tex * 128u * 4u &&
              p.pal_bytes >= p.tpal_off + 8u * SL * p.pal_stride * 4u);
   for (uint32_t i = tid; i < (uint32_t)(reinterpret_cast<uint8_t*>(bars) - smem) / 4; i += NWG * 128)
     reinterpret_cast<uint32_t*>(smem)[i] = 0x7FC17FC1u;   // poison: fp32 and fp16 NaN
@@ -344,18 +351,26 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
 
   // 16 grid features of row r (levels coarse->fine, 2 per level, R3) -> fp16 -> A columns 0..15 of slot sl
   auto features = [&](int g, float pu, float pv, float* dump, int sl) {
-    uint32_t hv[kMaxLevels];
+    uint32_t hv[kMaxLevels], lv[kMaxLevels];
 #pragma unroll
     for (int l = 0; l < kMaxLevels; l++) {
       float f0, f1;   // all levels unconditionally: unused ones are set up to return +0 (launch_fused)
       f2unpack(level_lookup2(p.blob, p.lv[g][l], pu, pv), f0, f1);
       if (dump) { dump[2 * l] = f0; dump[2 * l + 1] = f1; }
-      const __half2 v = __floats2half2_rn(f0, f1);
-      hv[l] = *reinterpret_cast<const uint32_t*>(&v);
+      if (SPLIT) {
+        split_h2(f0, f1, hv[l], lv[l]);
+      } else {
+        const __half2 v = __floats2half2_rn(f0, f1);
+        hv[l] = *reinterpret_cast<const uint32_t*>(&v);
+      }
     }
     uint8_t* As = A + sl * p.a_bytes;
-    *reinterpret_cast<uint4*>(As + kmajor_offset(r, 0, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-    *reinterpret_cast<uint4*>(As + kmajor_offset(r, 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+    *reinterpret_cast<uint4*>(As + kmajor_offset(r, 0, KA)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    *reinterpret_cast<uint4*>(As + kmajor_offset(r, 8, KA)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+    if (SPLIT) {
+      *reinterpret_cast<uint4*>(As + kmajor_offset(r, 16, KA)) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+      *reinterpret_cast<uint4*>(As + kmajor_offset(r, 24, KA)) = make_uint4(lv[4], lv[5], lv[6], lv[7]);
+    }
   };
 
   // layer l of net n on slot sl: the group's A rows are complete (barrier), one thread issues the MMAs
@@ -367,7 +382,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       tc_fence_after();
       const int kin16 = l == 0 ? 16 : H;
       const int N = l < 3 ? H : p.net[n].n_out16;
-      issue_layer(tm + sl * 64, a_base + sl * p.a_bytes, H, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
+      issue_layer<SPLIT>(tm + sl * 64, a_base + sl * p.a_bytes, KA, ones_base, img_base[n] + p.net[n].layer_off[l], kin16, N);
       mma_commit(bar_mma + sl);
     }
   };
@@ -389,7 +404,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     constexpr bool PF = NWG <= 4;   // prefetch the next chunk (16 more registers than NWG 8 has)
     const uint32_t tr = tm_row + sl * 64;
     uint8_t* As = A + sl * p.a_bytes;
-    if (NTBC_TMEM_PF8 && !PF) {     // 8-column chunks, the next chunk's load in flight during this chunk's selu
+    if (NTBC_TMEM_PF8 && !PF && !SPLIT) {     // 8-column chunks, the next chunk's load in flight during this chunk's selu
       uint32_t b8[2][8];
       tmem_ld8p(tr, b8[0]);
       tmem_wait_ld8(b8[0]);
@@ -416,11 +431,22 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       }
       if (PF && c + 1 < H / 16) tmem_ld16p(tr + (c + 1) * 16, buf[(c + 1) & 1]);
       uint32_t hv[8];
+      if (SPLIT) {   // contract F: binary32 selu, hi chunk at physical 2c, lo chunk at 2c + 1
+        uint32_t lv[8];
 #pragma unroll
-      for (int j = 0; j < 8; j++)
-        hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
-      *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-      *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+        for (int j = 0; j < 8; j++)
+          selu2_split(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]), hv[j], lv[j]);
+        *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 32, KA)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+        *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 32 + 8, KA)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+        *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 32 + 16, KA)) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+        *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 32 + 24, KA)) = make_uint4(lv[4], lv[5], lv[6], lv[7]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+          hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
+        *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+        *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+      }
       if (PF && c + 1 < H / 16) tmem_wait_ld16(buf[(c + 1) & 1]);
     }
   };

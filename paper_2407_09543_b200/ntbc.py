@@ -57,6 +57,7 @@ _SIGS = {
     "ntbc_peer_close": (_i, [_vp]),
     "ntbc_launch_count": (C.c_uint64, []),
     "ntbc_debug_time_fused": (_i, [_vp, _vp]),
+    "ntbc_set_contract": (_i, [_vp, _i]),
     "ntbc_last_error": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -318,3 +319,8 @@ def time_fused(start_event=None, end_event=None):
     a = start_event.cuda_event if start_event is not None else None
     b = end_event.cuda_event if end_event is not None else None
     _check(_lib.ntbc_debug_time_fused(a, b))
+
+
+def set_contract(model, contract: int):
+    """ntbc_set_contract: 0 = H (binary16 activations, the paper's), 1 = F (binary32 activations, hi/lo operands)."""
+    _check(_lib.ntbc_set_contract(model._h, int(contract)))

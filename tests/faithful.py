@@ -11,9 +11,16 @@ Rule (BASELINE.json north_star):
         the two codes, which differ by one step (P:106-115; R11);
       - index field (endpoints equal): the texel's plain colour c lies within 1e-4 of the bisector of
         the two chosen palette entries, (|c - c_b|^2 - |c - c_a|^2) / (2 |c_a - c_b|) < 1e-4 (Eq.9-10);
-  * reported by class: 5-bit / 6-bit / 8-bit endpoint, BC1 / BC4 index.
+  * reported by class: 5-bit / 6-bit / 8-bit endpoint, BC1 / BC4 index;
+  * index ties: when the two chosen palette entries are EQUAL in exact arithmetic (Eq. 7/8 with the stored
+    endpoints; e.g. a BC4 block with E0 == E1, whose 6-value entries 1..6 all equal E0/255 -- the binary32
+    palette separates them only by rounding noise), both codes decode to the same value of the definition,
+    so both are correct results (the order of equal keys); such words are counted as excused, class
+    `index_tie`.
 """
 from __future__ import annotations
+
+from fractions import Fraction
 
 import numpy as np
 
@@ -25,7 +32,28 @@ BAND = 1e-4
 _INV1 = {0: 0, 2: 1, 3: 2, 1: 3}
 _INV4_8 = {0: 0, 2: 1, 3: 2, 4: 3, 5: 4, 6: 5, 7: 6, 1: 7}
 _INV4_6 = {6: 0, 0: 1, 2: 2, 3: 3, 4: 4, 5: 5, 1: 6, 7: 7}
-CLASSES = ("endpoint5", "endpoint6", "endpoint8", "index_bc1", "index_bc4")
+CLASSES = ("endpoint5", "endpoint6", "endpoint8", "index_bc1", "index_bc4", "index_tie")
+
+
+def _exact_entry(fmt, hdr, n):
+    """Palette entry n (linear order) in exact rational arithmetic (Eq. 7 / Eq. 8, UNORM endpoints)."""
+    if fmt == BC1:
+        c0, c1 = hdr & 0xFFFF, (hdr >> 16) & 0xFFFF
+        e0 = [Fraction(c0 >> 11, 31), Fraction((c0 >> 5) & 63, 63), Fraction(c0 & 31, 31)]
+        e1 = [Fraction(c1 >> 11, 31), Fraction((c1 >> 5) & 63, 63), Fraction(c1 & 31, 31)]
+        w = Fraction(n, 3)
+        return tuple((1 - w) * a + w * b for a, b in zip(e0, e1))
+    E0, E1 = hdr & 0xFF, (hdr >> 8) & 0xFF
+    e0, e1 = Fraction(E0, 255), Fraction(E1, 255)
+    if E0 > E1:
+        w = Fraction(n, 7)
+    elif n == 0:
+        return (Fraction(0),)
+    elif n == 7:
+        return (Fraction(1),)
+    else:
+        w = Fraction(n - 1, 5)
+    return ((1 - w) * e0 + w * e1,)
 
 
 def float_stats(g, o):
@@ -79,8 +107,9 @@ def _palette(fmt, hdr):
     return oracle.palette_bc4(E0, E1).astype(np.float64)[:, None]
 
 
-def _index_excused(fmt, gw, pw, texels) -> bool:
-    """Index-only mismatch: every differing texel lies within 1e-4 of the bisector of the two entries."""
+def _index_excused(fmt, gw, pw, texels):
+    """Index-only mismatch: every differing texel lies within 1e-4 of the bisector of the two entries, or
+    the two entries are equal in exact arithmetic.  Returns (excused, all differences are such ties)."""
     if fmt == BC1:
         hdr, shift, bits, inv = pw & 0xFFFFFFFF, 32, 2, _INV1
     else:
@@ -88,11 +117,15 @@ def _index_excused(fmt, gw, pw, texels) -> bool:
         inv = _INV4_8 if (hdr & 0xFF) > ((hdr >> 8) & 0xFF) else _INV4_6
     pal = _palette(fmt, hdr)
     mask = (1 << bits) - 1
+    tie = True
     for i in range(16):
         cg = (gw >> (shift + bits * i)) & mask
         cp = (pw >> (shift + bits * i)) & mask
         if cg == cp:
             continue
+        if _exact_entry(fmt, hdr, inv[cp]) == _exact_entry(fmt, hdr, inv[cg]):
+            continue   # equal entries of the definition: both codes are correct
+        tie = False
         c = np.asarray(texels[i], np.float64).reshape(-1)
         a, b = pal[inv[cp]], pal[inv[cg]]
         sep = float(np.linalg.norm(a - b))
@@ -100,8 +133,8 @@ def _index_excused(fmt, gw, pw, texels) -> bool:
             continue   # coincident entries: an exact tie
         dist = (float(np.sum((c - b) ** 2)) - float(np.sum((c - a) ** 2))) / (2.0 * sep)
         if not dist < BAND:
-            return False
-    return True
+            return False, False
+    return True, tie
 
 
 def compare_words(fmts, gw, pw, pep, pcol, n_c_offsets=None, naive=False):
@@ -133,9 +166,9 @@ def compare_words(fmts, gw, pw, pep, pcol, n_c_offsets=None, naive=False):
                         if gv != pv:
                             ok &= _near_mid(e[j], 255, gv, pv)
             else:
-                cls = "index_bc1" if f == BC1 else "index_bc4"
                 tex = [pcol[4 * r + (i >> 2), 4 * bx + (i & 3), co:co + w] for i in range(16)]
-                ok = _index_excused(f, G, P, tex)
+                ok, tie = _index_excused(f, G, P, tex)
+                cls = "index_tie" if tie else "index_bc1" if f == BC1 else "index_bc4"
             rep["mismatched"] += 1
             rep["excused" if ok else "unexcused"] += 1
             rep[cls][0 if ok else 1] += 1

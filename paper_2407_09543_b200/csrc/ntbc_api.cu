@@ -1131,15 +1131,28 @@ ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static void (*const kernels[kMaxTex])(PackParams) = {pack_kernel<1>, pack_kernel<2>, pack_kernel<3>, pack_kernel<4>,
                                                        pack_kernel<5>, pack_kernel<6>, pack_kernel<7>, pack_kernel<8>};
+  static void (*const kernels_bt[kMaxTex])(PackParams) = {pack_kernel_bt<1>, pack_kernel_bt<2>, pack_kernel_bt<3>,
+                                                          pack_kernel_bt<4>, pack_kernel_bt<5>, pack_kernel_bt<6>,
+                                                          pack_kernel_bt<7>, pack_kernel_bt<8>};
   static_assert(kMaxTex == 8, "pack kernel instantiations");
-  const auto kern = kernels[n_tex - 1];
+  // default: one thread per (block, texture) (pack_kernel_bt); NTBC_PACK_WARP=1: the warp-per-two-blocks form
+  const bool warp_form = getenv("NTBC_PACK_WARP") && atoi(getenv("NTBC_PACK_WARP"));
+  const auto kern = warp_form ? kernels[n_tex - 1] : kernels_bt[n_tex - 1];
+  const int threads = warp_form ? kPackThreads : kBtTile * n_tex;
+  const size_t smem_k = warp_form ? smem : (384 + (size_t)kBtStages * (4 * (size_t)(4 * kBtTile * p.n_c) +
+                                                                        (size_t)((kBtTile * p.n_e + 3) & ~3))) * sizeof(float) +
+                                            8 * kBtStages;
   CUDA_TRY(allow_smem((const void*)kern, 227 * 1024));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPackThreads, smem));
+  // the whole unified L1 as shared memory: several CTAs of staged tiles per SM
+  CUDA_TRY(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem_k));
   // persistent grid: exactly the resident CTAs (a second partial wave of grid-stride CTAs would double
-  // the tail), each striding over 16-block tiles
-  const int grid = std::max(1, std::min(p.n_tiles, sms * std::max(per_sm, 1)));
-  if (smem > 227 * 1024) return fail(NTBC_EINVAL, "pack tile needs %zu B of shared memory", smem);
-  kern<<<grid, kPackThreads, smem, (cudaStream_t)stream>>>(p);
+  // the tail), each striding over 64-block tiles
+  const int n_tiles = warp_form ? p.n_tiles : (p.BW + kBtTile - 1) / kBtTile * p.rows;
+  const int grid = std::max(1, std::min(n_tiles, sms * std::max(per_sm, 1)));
+  if (smem_k > 227 * 1024) return fail(NTBC_EINVAL, "pack tile needs %zu B of shared memory", smem_k);
+  kern<<<grid, threads, smem_k, (cudaStream_t)stream>>>(p);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return NTBC_OK;

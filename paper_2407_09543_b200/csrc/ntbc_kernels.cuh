@@ -865,6 +865,150 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
   }
 }
 
+// Kernel (2), thread-per-(block, texture) form (the default since r02): 64 x NT threads per CTA, thread
+// j = k * 64 + b owns texture k of block b of the tile.  It quantizes the block's endpoints (R11-R13), builds
+// the palette ONCE in registers (Eq.7/8, R18), then walks the block's 16 texels (argmin of Eq.9-10, R14/R15)
+// accumulating the index field with shifts -- no per-texel palette rebuild, no warp reductions -- and stores
+// its word; the 32 lanes of a warp hold 32 consecutive blocks of one texture, so the stores are coalesced
+// (even lanes write two adjacent words as one 16-byte store when p.vec16).  Same tile staging (cp.async) as
+// pack_kernel.
+#ifndef NTBC_PACK_BT_THREADS
+#define NTBC_PACK_BT_THREADS 1280   // launch-bounds target of resident threads per SM (register budget)
+#endif
+#ifndef NTBC_PACK_BT_TILE
+#define NTBC_PACK_BT_TILE 32    // block positions per tile of pack_kernel_bt (threads = tile x textures); C3 A/B
+                                // r02v/w: 32 -> 0.156 ms (0.707 of HBM), 64 -> 0.164, 128 -> 0.174, 16 -> 0.182
+#endif
+#ifndef NTBC_PACK_BT_STAGES
+#define NTBC_PACK_BT_STAGES 1   // 2: the next tile's bulk copies in flight during this tile's work (r02t: slower,
+                                // 0.172 vs 0.164 ms -- half the CTAs per SM; 32-block tiles x 2 stages 0.176)
+#endif
+constexpr int kBtTile = NTBC_PACK_BT_TILE, kBtStages = NTBC_PACK_BT_STAGES;
+// min blocks per SM = 1,280 threads' worth: <= 51 registers (four 320-thread CTAs for C3)
+template <int NT>
+__global__ void __launch_bounds__(kBtTile * NT, (NTBC_PACK_BT_THREADS / (kBtTile * NT)) > 2 ? (NTBC_PACK_BT_THREADS / (kBtTile * NT)) : 2)
+    pack_kernel_bt(const __grid_constant__ PackParams p) {
+  extern __shared__ __align__(16) float psm[];
+  float* s_unorm = psm;                                   // 352 UNORM quotients + 32 BC4 weights
+  const int rs = 4 * kBtTile * p.n_c;                     // texel-row stride of a staged tile (floats)
+  const int ep_floats = (kBtTile * p.n_e + 3) & ~3;
+  const int stage_floats = 4 * rs + ep_floats;            // one stage: [4][4 tile N_c] colours, [tile][N_e] endpoints
+  uint64_t* bar = reinterpret_cast<uint64_t*>(psm + 384 + kBtStages * stage_floats);   // one per stage
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int k = tid / kBtTile, b = tid - k * kBtTile;     // texture, block of the tile
+  for (int i = tid; i < 352; i += blockDim.x)
+    s_unorm[i] = i < 32 ? __fdiv_rn((float)i, 31.0f) : i < 96 ? __fdiv_rn((float)(i - 32), 63.0f)
+                                                            : __fdiv_rn((float)(i - 96), 255.0f);
+  if (tid < 32) s_unorm[352 + tid] = bc4_weight(tid);
+  if (tid == 0) {
+    for (int q = 0; q < kBtStages; q++) mbar_init(bar + q, 1);
+    fence_mbar_init();
+  }
+#if NTBC_CHECKS
+  NTBC_CHECK((uint32_t)(reinterpret_cast<uint8_t*>(bar + kBtStages) - reinterpret_cast<uint8_t*>(psm)) <= dyn_smem_bytes());
+  for (int i = 384 + tid; i < 384 + kBtStages * stage_floats; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(psm)[i] = 0x7FC17FC1u;   // poison the staging buffers
+  fence_async_smem();
+#endif
+  __syncthreads();
+  // per-texture parameters of this thread (k is warp-uniform: kBtTile threads per texture)
+  const int fmt = p.fmt[k], eo = p.ep_off[k], co = p.col_off[k];
+  uint64_t* const out = p.out[k];
+  const int tpr = (p.BW + kBtTile - 1) / kBtTile, n_tiles = tpr * p.rows;
+  // the tile's fp32 MLP outputs: 4 texel-row segments (16-B aligned, 16 nb N_c bytes each) and the endpoints,
+  // by bulk asynchronous copies (TMA engine) issued by one thread into stage q; the endpoints by plain loads
+  // of all threads when their segment is not 16-B aligned (N_e x the block index odd)
+  auto issue = [&](int t, int q) {   // thread 0 only
+    const int row = t / tpr, bx0 = (t - row * tpr) * kBtTile, nb = min(kBtTile, p.BW - bx0);
+    float* s_col = psm + 384 + q * stage_floats;
+    const float* ep_src = p.ep + ((size_t)row * p.BW + bx0) * p.n_e;
+    const uint32_t ep_bytes = (uint32_t)(nb * p.n_e * 4), row_bytes = (uint32_t)(16 * nb * p.n_c);
+    const bool ep_bulk = ((((uintptr_t)ep_src) | ep_bytes) & 15) == 0;
+    mbar_arrive_expect_tx(bar + q, 4 * row_bytes + (ep_bulk ? ep_bytes : 0));
+    for (int yi = 0; yi < 4; yi++)
+      bulk_g2s(s_col + yi * rs, p.col + ((size_t)(4 * row + yi) * p.W + 4 * bx0) * p.n_c, row_bytes, bar + q);
+    if (ep_bulk) bulk_g2s(s_col + 4 * rs, ep_src, ep_bytes, bar + q);
+  };
+  uint32_t phase[kBtStages];
+  for (int q = 0; q < kBtStages; q++) phase[q] = 0;
+  if (tid == 0 && (int)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, it++) {
+    const int q = kBtStages > 1 ? (it & 1) : 0;
+    const int row = t / tpr, bx0 = (t - row * tpr) * kBtTile;
+    const int nb = min(kBtTile, p.BW - bx0);
+    float* s_col = psm + 384 + q * stage_floats;           // [4][4 tile N_c]
+    float* s_ep = s_col + 4 * rs;                          // [tile][N_e]
+    const float* ep_src = p.ep + ((size_t)row * p.BW + bx0) * p.n_e;
+    const bool ep_bulk = ((((uintptr_t)ep_src) | (uint32_t)(nb * p.n_e * 4)) & 15) == 0;
+    if (kBtStages > 1) {
+      __syncthreads();   // every thread is done with the other stage (the previous tile)
+      if (tid == 0 && t + (int)gridDim.x < n_tiles) issue(t + gridDim.x, q ^ 1);
+    } else if (it > 0) {
+      __syncthreads();   // every thread is done with the stage
+      if (tid == 0) issue(t, 0);
+    }
+    if (!ep_bulk) {
+      if (kBtStages == 1) __syncthreads();
+      for (int i = tid; i < nb * p.n_e; i += blockDim.x) s_ep[i] = ep_src[i];
+      __syncthreads();
+    }
+    mbar_wait(bar + q, phase[q]);
+    phase[q] ^= 1u;
+    const int bb = min(b, nb - 1);
+    const float* e = s_ep + bb * p.n_e + eo;
+    const float* c = s_col + 4 * bb * p.n_c + co;        // texel (x, y) of the block at c + y rs + x n_c
+    uint64_t word;
+    if (fmt == kFmtBC1) {
+      float ep6[6];
+#pragma unroll
+      for (int j = 0; j < 6; j++) ep6[j] = e[j];
+      bool swapped;
+      const uint32_t hdr = quant_bc1_hdr(ep6, swapped);
+      const uint32_t c0 = hdr & 0xFFFFu, c1 = hdr >> 16;
+      const float e0[3] = {s_unorm[c0 >> 11], s_unorm[32 + ((c0 >> 5) & 63)], s_unorm[c0 & 31]};
+      const float e1[3] = {s_unorm[c1 >> 11], s_unorm[32 + ((c1 >> 5) & 63)], s_unorm[c1 & 31]};
+      float pal[12];
+      bc1_palette_pairs(e0, e1, pal);
+      const bool degenerate = c0 == c1;
+      uint32_t bits = 0;
+#pragma unroll
+      for (int i = 0; i < 16; i++) {
+        const float* ci = c + (i >> 2) * rs + (i & 3) * p.n_c;
+        const float cc[3] = {ci[0], ci[1], ci[2]};
+        bits |= bc1_code_pairs(cc, reinterpret_cast<const float2*>(pal), degenerate) << (2 * i);
+      }
+      word = (uint64_t)hdr | ((uint64_t)bits << 32);
+    } else {
+      const float ep2[2] = {e[0], e[1]};
+      const uint32_t hdr = quant_bc4_hdr(ep2);
+      const uint32_t E0 = hdr & 0xFFu, E1 = (hdr >> 8) & 0xFFu;
+      float pl[8];
+      bc4_palette_tab(s_unorm[96 + E0], s_unorm[96 + E1], E0 > E1, s_unorm + 352, pl);
+      uint64_t bits = 0;
+      if (E0 != E1) {   // strictly monotone palette: the one-select argmin (bc4_code_mono)
+#pragma unroll
+        for (int i = 0; i < 16; i++)
+          bits |= (uint64_t)bc4_code_mono(c[(i >> 2) * rs + (i & 3) * p.n_c], pl, E0 > E1) << (3 * i);
+      } else {
+#pragma unroll 1
+        for (int i = 0; i < 16; i++)
+          bits |= (uint64_t)bc4_code(c[(i >> 2) * rs + (i & 3) * p.n_c], pl, false) << (3 * i);
+      }
+      word = (uint64_t)hdr | (bits << 16);
+    }
+    const size_t oidx = (size_t)row * p.BW + bx0 + b;
+    if (p.vec16) {   // b even: this lane and the next hold two adjacent words -> one 16-byte store
+      const uint64_t next = __shfl_down_sync(0xFFFFFFFFu, word, 1);
+      NTBC_CHECK(!((lane & 1) == 0 && b < nb) || (bx0 + b < p.BW && row < p.rows));
+      if ((lane & 1) == 0 && b + 1 < nb) st_words2(out + oidx, word, next);
+      else if ((lane & 1) == 0 && b < nb) out[oidx] = word;
+    } else if (b < nb) {
+      out[oidx] = word;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- kernel (3): BC decode (a9)
 __global__ void __launch_bounds__(256) decode_bc_kernel(const uint64_t* __restrict__ blocks, int fmt, int W, int H,
                                                          float* __restrict__ out) {

@@ -466,3 +466,40 @@ def test_odd_coarsest_resolutions(ntbc, block_coarsest, texel_coarsest):
         s_ = np.float32((np.float32(bx) + np.float32(0.5)) / np.float32(W // 4))
         t = np.float32(np.float32(1.5) / np.float32(H // 4))
         assert np.array_equal(bf[1, bx, :6].view(np.uint32), om.grid_encode(0, float(s_), float(t)).view(np.uint32))
+
+
+def test_pack_bc4_ties_and_monotone_argmin(ntbc):
+    """The pack kernel's one-select BC4 argmin (bc4_code_mono, valid for E0 != E1) against the oracle's
+    strict-< scan on adversarial texels: every midpoint between adjacent binary32 palette entries and its two
+    neighbouring floats, for endpoint pairs including E0 = 0, E1 = 255 (Eq. 8's constants equal to an
+    endpoint), E0 = E1 +- 1 and E0 = E1 (the exact-scan fallback), both modes."""
+    rng = np.random.default_rng(5)
+    pairs = [(0, 0), (255, 255), (0, 255), (255, 0), (0, 1), (1, 0), (254, 255), (255, 254), (52, 52), (200, 10)]
+    pairs += [tuple(int(v) for v in rng.integers(0, 256, 2)) for _ in range(54)]
+    blocks_ep, texels = [], []
+    for E0, E1 in pairs:
+        pal = oracle.palette_bc4(E0, E1).astype(np.float32)
+        vals = []
+        for n in range(7):
+            mid = np.float32((np.float64(pal[n]) + np.float64(pal[n + 1])) / 2)
+            vals += [mid, np.nextafter(mid, np.float32(-1)), np.nextafter(mid, np.float32(2))]
+        vals += list(pal) + [np.float32(0), np.float32(1), np.float32(0.5)]
+        vals = np.array(vals, np.float32)
+        for j in range(0, len(vals), 16):
+            t = vals[j:j + 16]
+            t = np.concatenate([t, rng.uniform(0, 1, 16 - t.size).astype(np.float32)]) if t.size < 16 else t
+            blocks_ep.append([np.float32(E0) / np.float32(255), np.float32(E1) / np.float32(255)])
+            texels.append(t)
+    nb = len(blocks_ep)
+    BW = nb                               # one block row
+    ep = np.array(blocks_ep, np.float32).reshape(1, BW, 2)
+    col = np.zeros((4, 4 * BW, 1), np.float32)
+    for b, t in enumerate(texels):
+        for i in range(16):
+            col[i >> 2, 4 * b + (i & 3), 0] = t[i]
+    W, H = 4 * BW, 4
+    o = oracle.pack([4], ep, col, W, H)
+    assert all(((int(w) & 0xFF) == E0 and ((int(w) >> 8) & 0xFF) == E1)
+               for w, (E0, E1) in zip(o[0][0][::3], [(int(round(e[0] * 255)), int(round(e[1] * 255))) for e in blocks_ep[::3]]))
+    g = ntbc.pack([4], torch.from_numpy(ep).to(DEV), torch.from_numpy(col).to(DEV), W, H)
+    assert np.array_equal(u64(g[0]), o[0])

@@ -28,6 +28,11 @@ namespace ntbc {
                            // full-size digests -- but slower, A/B r02j: 2.575 vs 2.201 ms: 16 warps per SM
                            // hide less latency than 32)
 #endif
+#ifndef NTBC_EPI_JOBS
+#define NTBC_EPI_JOBS 1    // colour tile's index selection + packing: 0 = every thread its texel of every texture
+                           // (round 1); 1 = (texture, block, half) jobs after a group barrier (A/B r02x: 2.174 vs
+                           // 2.201 ms); 2 = warp-local jobs without the barrier (r02y: 2.250, slower)
+#endif
 #ifndef NTBC_TMEM_PF8
 #define NTBC_TMEM_PF8 0    // 1: hidden epilogue loads TMEM in 8-column chunks with the next chunk in flight (same
                            // registers as the x16 loads; A/B r02l: 2.214 vs 2.197 ms, slower -- the TMEM load
@@ -527,6 +532,114 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
     // ================= colour tiles: row r = texel (r & 15) of block 8j + (r >> 4)  (a1-a2, a4, a6-a8)
     // index selection + packing of colour tile jt from slot sl's staged outputs (the block palettes at
     // tpal[8 sl + r / 16] were built at the tile start)
+    // index selection + packing of colour tile jt by JOBS: thread r takes half h = r & 1 (texels 8h..8h+7) of
+    // job r >> 1 = (texture, block) -- BC1 textures first, then BC4, 8 blocks each -- reading the tile's
+    // staged outputs of its block (8 consecutive rows: vector loads), the block's palette built at the tile
+    // start, and combining the two halves' index fields with one shuffle; the even thread stores the word.
+    // Each (block, texture) palette and header is read once per half instead of once per texel (the
+    // per-texel form, pack_tile, costs every thread the whole texture loop).
+    auto pack_tile_jobs = [&](int jt, int sl) {
+      named_bar_sync(bar_id, 128);                       // every row's outputs are staged
+      const float* st = reinterpret_cast<const float*>(A + sl * p.a_bytes);
+      const int job = r >> 1, h = r & 1;
+      const int nj = 8 * p.n_tex;
+      const int jj = min(job, nj - 1);                   // idle threads shadow the last job (no store)
+      const int ti = jj >> 3, bl = jj & 7;               // texture slot (BC1 list then BC4 list), block
+      const bool bc1 = ti < p.n_bc1;
+      const int k = bc1 ? p.tex_bc1[ti] : p.tex_bc4[ti - p.n_bc1];
+      const int co = p.col_off[k];
+      const int b = 8 * jt + bl;
+      const uint32_t hdr = hdrs[k * 128 + b];
+      const float* tp = tpal + (8 * sl + bl) * p.pal_stride + p.pal_off[k];
+      const int row0 = 16 * bl + 8 * h;                  // this half's first texel row in the stage
+      uint64_t bits;
+      if (bc1) {
+        const float2* P = reinterpret_cast<const float2*>(tp);
+        const bool degenerate = (hdr & 0xFFFFu) == (hdr >> 16);
+        float cr[8], cg[8], cb[8];
+        *reinterpret_cast<float4*>(cr) = *reinterpret_cast<const float4*>(st + co * 128 + row0);
+        *reinterpret_cast<float4*>(cr + 4) = *reinterpret_cast<const float4*>(st + co * 128 + row0 + 4);
+        *reinterpret_cast<float4*>(cg) = *reinterpret_cast<const float4*>(st + (co + 1) * 128 + row0);
+        *reinterpret_cast<float4*>(cg + 4) = *reinterpret_cast<const float4*>(st + (co + 1) * 128 + row0 + 4);
+        *reinterpret_cast<float4*>(cb) = *reinterpret_cast<const float4*>(st + (co + 2) * 128 + row0);
+        *reinterpret_cast<float4*>(cb + 4) = *reinterpret_cast<const float4*>(st + (co + 2) * 128 + row0 + 4);
+        uint32_t v = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const float c[3] = {cr[i], cg[i], cb[i]};
+          v |= bc1_code_pairs(c, P, degenerate) << (2 * i);
+        }
+        const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+        bits = (uint64_t)(v | (o << 16)) << 32;
+      } else {
+        const float4 q0 = reinterpret_cast<const float4*>(tp)[0], q1 = reinterpret_cast<const float4*>(tp)[1];
+        const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const bool mode8 = (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu);
+        float cv[8];
+        *reinterpret_cast<float4*>(cv) = *reinterpret_cast<const float4*>(st + co * 128 + row0);
+        *reinterpret_cast<float4*>(cv + 4) = *reinterpret_cast<const float4*>(st + co * 128 + row0 + 4);
+        uint32_t v = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) v |= bc4_code(cv[i], pl, mode8) << (3 * i);
+        const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+        bits = (uint64_t)(v | ((uint64_t)o << 24)) << 16;
+      }
+      if (h == 0 && job < nj && b < nvalid) {
+        NTBC_CHECK(bx0 + b < p.BW && by < p.row_end);
+        p.out[k][out_row + bx0 + b] = (uint64_t)hdr | bits;
+      }
+    };
+    // the same work by WARP-LOCAL jobs (NTBC_EPI_JOBS=2): warp w of the group staged rows 32w..32w+31 = the
+    // texels of blocks 2w and 2w+1 of the tile, so it packs exactly those two blocks -- no group barrier, only
+    // __syncwarp.  The BC1 jobs (2 blocks x n_bc1 textures) and then the BC4 jobs (2 x n_bc4) each spread
+    // over the warp: lpj = 32 / jobs lanes per job (a power of two), 16 / lpj texels per lane, the job's
+    // index field OR-combined over its lanes with shuffles; the job's first lane stores the word.
+    auto pack_tile_warp = [&](int jt, int sl) {
+      __syncwarp();
+      const float* st = reinterpret_cast<const float*>(A + sl * p.a_bytes);
+      const int wq = (r >> 5) & 3;                        // warp of the group: blocks 2 wq, 2 wq + 1
+      for (int fmt_pass = 0; fmt_pass < 2; fmt_pass++) {
+        const bool bc1 = fmt_pass == 0;
+        const int ntx = bc1 ? p.n_bc1 : p.n_bc4;
+        if (ntx == 0) continue;
+        const int nj = 2 * ntx;
+        const int lpj = nj <= 2 ? 16 : nj <= 4 ? 8 : nj <= 8 ? 4 : nj <= 16 ? 2 : 1;
+        const int tpl = 16 / lpj;
+        const int job = lane / lpj, part = lane - job * lpj;
+        const int jj = min(job, nj - 1);
+        const int ti = jj >> 1, bl = 2 * wq + (jj & 1);
+        const int k = bc1 ? p.tex_bc1[ti] : p.tex_bc4[ti];
+        const int co = p.col_off[k];
+        const int b = 8 * jt + bl;
+        const uint32_t hdr = hdrs[k * 128 + b];
+        const float* tp = tpal + (8 * sl + bl) * p.pal_stride + p.pal_off[k];
+        const int t0 = part * tpl;                         // this lane's first texel of the block
+        const float* sr = st + 16 * bl + t0;               // texel t0's row in the stage
+        uint64_t bits = 0;
+        if (bc1) {
+          const float2* P = reinterpret_cast<const float2*>(tp);
+          const bool degenerate = (hdr & 0xFFFFu) == (hdr >> 16);
+          for (int i = 0; i < tpl; i++) {
+            const float c[3] = {sr[co * 128 + i], sr[(co + 1) * 128 + i], sr[(co + 2) * 128 + i]};
+            bits |= (uint64_t)bc1_code_pairs(c, P, degenerate) << (2 * (t0 + i));
+          }
+        } else {
+          const float4 q0 = reinterpret_cast<const float4*>(tp)[0], q1 = reinterpret_cast<const float4*>(tp)[1];
+          const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          const bool mode8 = (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu);
+          for (int i = 0; i < tpl; i++) bits |= (uint64_t)bc4_code(sr[co * 128 + i], pl, mode8) << (3 * (t0 + i));
+        }
+        for (int d = 1; d < lpj; d <<= 1) {                // OR over the job's lanes (disjoint fields)
+          const uint32_t lo = __shfl_xor_sync(0xFFFFFFFFu, (uint32_t)bits, d);
+          const uint32_t hi = __shfl_xor_sync(0xFFFFFFFFu, (uint32_t)(bits >> 32), d);
+          bits |= (uint64_t)hi << 32 | lo;
+        }
+        if (part == 0 && job < nj && b < nvalid) {
+          NTBC_CHECK(bx0 + b < p.BW && by < p.row_end);
+          p.out[k][out_row + bx0 + b] = (uint64_t)hdr | (bits << (bc1 ? 32 : 16));
+        }
+      }
+    };
     auto pack_tile = [&](int jt, int sl) {
       const int b = 8 * jt + (r >> 4);
       const int bx = bx0 + b;
@@ -640,7 +753,11 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
           for (int ch = 0; ch < p.net[1].n_out; ch++)
             p.dump_col[(((size_t)(y - 4 * p.row_begin)) * p.W + x) * p.net[1].n_out + ch] = stage[ch * 128 + r];
       } else {
-        for (int sl = 0; sl < ntile; sl++) pack_tile(j + sl, sl);
+        for (int sl = 0; sl < ntile; sl++) {
+          if (NTBC_EPI_JOBS == 2 && !NAIVE) pack_tile_warp(j + sl, sl);
+          else if (NTBC_EPI_JOBS == 1 && !NAIVE) pack_tile_jobs(j + sl, sl);
+          else pack_tile(j + sl, sl);
+        }
       }
     }
     if (!DUMP && p.progress) {  // publish the finished unit: group barrier, then one system-scope release

@@ -754,8 +754,10 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
             p.dump_col[(((size_t)(y - 4 * p.row_begin)) * p.W + x) * p.net[1].n_out + ch] = stage[ch * 128 + r];
       } else {
         for (int sl = 0; sl < ntile; sl++) {
+          // jobs pay with >= 3 textures (>= 48 busy threads); with 1-2 textures the per-texel form keeps all four
+          // warps busy (tab1 r02ev: 2 BC1 textures 2.08 ms with jobs vs 1.99 per texel)
           if (NTBC_EPI_JOBS == 2 && !NAIVE) pack_tile_warp(j + sl, sl);
-          else if (NTBC_EPI_JOBS == 1 && !NAIVE) pack_tile_jobs(j + sl, sl);
+          else if (NTBC_EPI_JOBS == 1 && !NAIVE && p.n_tex >= 3) pack_tile_jobs(j + sl, sl);
           else pack_tile(j + sl, sl);
         }
       }

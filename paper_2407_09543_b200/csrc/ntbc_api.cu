@@ -1136,7 +1136,8 @@ ntbc_status ntbc_pack(int n_tex, const int* fmts, const float* endpoints, const 
                                                           pack_kernel_bt<7>, pack_kernel_bt<8>};
   static_assert(kMaxTex == 8, "pack kernel instantiations");
   // default: one thread per (block, texture) (pack_kernel_bt); NTBC_PACK_WARP=1: the warp-per-two-blocks form
-  const bool warp_form = getenv("NTBC_PACK_WARP") && atoi(getenv("NTBC_PACK_WARP"));
+  // (the bulk copies of the thread form need 16-B aligned colour rows: a misaligned `colors` takes the warp form)
+  const bool warp_form = (getenv("NTBC_PACK_WARP") && atoi(getenv("NTBC_PACK_WARP"))) || ((uintptr_t)colors & 15);
   const auto kern = warp_form ? kernels[n_tex - 1] : kernels_bt[n_tex - 1];
   const int threads = warp_form ? kPackThreads : kBtTile * n_tex;
   const size_t smem_k = warp_form ? smem : (384 + (size_t)kBtStages * (4 * (size_t)(4 * kBtTile * p.n_c) +

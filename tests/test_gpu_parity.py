@@ -503,3 +503,18 @@ def test_pack_bc4_ties_and_monotone_argmin(ntbc):
                for w, (E0, E1) in zip(o[0][0][::3], [(int(round(e[0] * 255)), int(round(e[1] * 255))) for e in blocks_ep[::3]]))
     g = ntbc.pack([4], torch.from_numpy(ep).to(DEV), torch.from_numpy(col).to(DEV), W, H)
     assert np.array_equal(u64(g[0]), o[0])
+
+
+def test_pack_misaligned_inputs(ntbc):
+    """ntbc_pack with a colour array that is only 4-B aligned (the bulk-copy form needs 16 B: the library falls
+    back to the warp form) and an odd block count (8-byte stores), against the oracle."""
+    fmts = [synth.BC1, synth.BC4, synth.BC4]
+    ep, col = synth.pack_inputs(fmts, 37, 5, seed=3)
+    W, H = 4 * 37, 4 * 5
+    buf = torch.empty(col.size + 1, dtype=torch.float32, device=DEV)
+    buf[1:] = torch.from_numpy(col.reshape(-1)).to(DEV)
+    col_d = buf[1:].view(col.shape)
+    g = ntbc.pack(fmts, torch.from_numpy(ep).to(DEV), col_d, W, H)
+    o = oracle.pack(fmts, ep, col, W, H)
+    for k in range(len(fmts)):
+        assert np.array_equal(u64(g[k]), o[k]), k

@@ -591,6 +591,57 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
         p.out[k][out_row + bx0 + b] = (uint64_t)hdr | bits;
       }
     };
+    // the same work by WARP-LOCAL jobs (NTBC_EPI_JOBS=2): warp w of the group staged rows 32w..32w+31 = the
+    // texels of blocks 2w and 2w+1 of the tile, so it packs exactly those two blocks -- no group barrier, only
+    // __syncwarp.  The BC1 jobs (2 blocks x n_bc1 textures) and then the BC4 jobs (2 x n_bc4) each spread
+    // over the warp: lpj = 32 / jobs lanes per job (a power of two), 16 / lpj texels per lane, the job's
+    // index field OR-combined over its lanes with shuffles; the job's first lane stores the word.
+    auto pack_tile_warp = [&](int jt, int sl) {
+      __syncwarp();
+      const float* st = reinterpret_cast<const float*>(A + sl * p.a_bytes);
+      const int wq = (r >> 5) & 3;                        // warp of the group: blocks 2 wq, 2 wq + 1
+      for (int fmt_pass = 0; fmt_pass < 2; fmt_pass++) {
+        const bool bc1 = fmt_pass == 0;
+        const int ntx = bc1 ? p.n_bc1 : p.n_bc4;
+        if (ntx == 0) continue;
+        const int nj = 2 * ntx;
+        const int lpj = nj <= 2 ? 16 : nj <= 4 ? 8 : nj <= 8 ? 4 : nj <= 16 ? 2 : 1;
+        const int tpl = 16 / lpj;
+        const int job = lane / lpj, part = lane - job * lpj;
+        const int jj = min(job, nj - 1);
+        const int ti = jj >> 1, bl = 2 * wq + (jj & 1);
+        const int k = bc1 ? p.tex_bc1[ti] : p.tex_bc4[ti];
+        const int co = p.col_off[k];
+        const int b = 8 * jt + bl;
+        const uint32_t hdr = hdrs[k * 128 + b];
+        const float* tp = tpal + (8 * sl + bl) * p.pal_stride + p.pal_off[k];
+        const int t0 = part * tpl;                         // this lane's first texel of the block
+        const float* sr = st + 16 * bl + t0;               // texel t0's row in the stage
+        uint64_t bits = 0;
+        if (bc1) {
+          const float2* P = reinterpret_cast<const float2*>(tp);
+          const bool degenerate = (hdr & 0xFFFFu) == (hdr >> 16);
+          for (int i = 0; i < tpl; i++) {
+            const float c[3] = {sr[co * 128 + i], sr[(co + 1) * 128 + i], sr[(co + 2) * 128 + i]};
+            bits |= (uint64_t)bc1_code_pairs(c, P, degenerate) << (2 * (t0 + i));
+          }
+        } else {
+          const float4 q0 = reinterpret_cast<const float4*>(tp)[0], q1 = reinterpret_cast<const float4*>(tp)[1];
+          const float pl[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          const bool mode8 = (hdr & 0xFFu) > ((hdr >> 8) & 0xFFu);
+          for (int i = 0; i < tpl; i++) bits |= (uint64_t)bc4_code(sr[co * 128 + i], pl, mode8) << (3 * (t0 + i));
+        }
+        for (int d = 1; d < lpj; d <<= 1) {                // OR over the job's lanes (disjoint fields)
+          const uint32_t lo = __shfl_xor_sync(0xFFFFFFFFu, (uint32_t)bits, d);
+          const uint32_t hi = __shfl_xor_sync(0xFFFFFFFFu, (uint32_t)(bits >> 32), d);
+          bits |= (uint64_t)hi << 32 | lo;
+        }
+        if (part == 0 && job < nj && b < nvalid) {
+          NTBC_CHECK(bx0 + b < p.BW && by < p.row_end);
+          p.out[k][out_row + bx0 + b] = (uint64_t)hdr | (bits << (bc1 ? 32 : 16));
+        }
+      }
+    };
     auto pack_tile = [&](int jt, int sl) {
       const int b = 8 * jt + (r >> 4);
       const int bx = bx0 + b;

@@ -69,6 +69,21 @@ def main():
             got = u64(buf[k])[off:off + rows * bw].reshape(rows, bw)
             assert np.array_equal(got, ref[k]), ("fuzz", w, hh, k)
             h.update(got.tobytes())
+    # contract F (binary32 activations, hi/lo split operands) on seeded random non-naive models, vs the oracle's F mode
+    n_f = 0
+    for blob, w, hh, r0, r1, misalign in fuzz_cases(40, seed=91):
+        om = oracle.Model(blob)
+        if om.naive or n_f >= 8:
+            continue
+        n_f += 1
+        m = ntbc.Model(blob)
+        ntbc.set_contract(m, 1)
+        outs = ntbc.decode_material([m], w, hh, row_begin=r0, row_end=r1)
+        with oracle.contract_f():
+            ref = om.decode_material(w, hh, r0, r1)
+        for k in range(m.n_tex):
+            assert np.array_equal(u64(outs[k]), ref[k]), ("contract F", w, hh, k)
+            h.update(u64(outs[k]).tobytes())
     # conservative pair (one launch, CTAs partitioned by model)
     rgb = synth.serialize(synth.random_model(synth.ModelSpec([synth.BC1, synth.BC1], block_levels=4, texel_levels=5), 5))
     sc = synth.serialize(synth.random_model(synth.ModelSpec([synth.BC4] * 4, block_levels=4, texel_levels=5), 6))
@@ -77,6 +92,14 @@ def main():
     for k in range(6):
         assert np.array_equal(u64(outs[k]), ref[k]), ("pair", k)
         h.update(u64(outs[k]).tobytes())
+    mr, ms = ntbc.Model(rgb), ntbc.Model(sc)          # the same pair under contract F (one launch)
+    ntbc.set_contract(mr, 1)
+    ntbc.set_contract(ms, 1)
+    outs = ntbc.decode_material([mr, ms], 256, 64)
+    with oracle.contract_f():
+        ref = list(oracle.Model(rgb).decode_material(256, 64)) + list(oracle.Model(sc).decode_material(256, 64))
+    for k in range(6):
+        assert np.array_equal(u64(outs[k]), ref[k]), ("pair F", k)
     # the standalone pack kernel
     for fmts, BW, BH in (([1, 1, 4, 4, 4], 41, 13), ([4], 1, 1), ([1] * 4 + [4] * 4, 130, 3)):
         ep, col = synth.pack_inputs(fmts, BW, BH, seed=BW * 31 + BH)

@@ -74,8 +74,10 @@ ntbc_status ntbc_model_upload_async(ntbc_model m, const void* blob, size_t nbyte
 ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out);
 void ntbc_free_model(ntbc_model m);                     /* NULL ok; caller guarantees no in-flight use */
 
-/* Rows a1-a8 of SURVEY §8, two launches per model: the grid dequantization (Eq.2; every level's
- * codes -> fp32 in the model's weight slot), then one fused sm_100a kernel: bilinear sampling
+/* Rows a1-a8 of SURVEY §8: per model a prep launch -- the grid dequantization (Eq.2; every level's
+ * codes -> fp32 in the model's weight slot) and the fused kernel's shared-memory prefix image (tcgen05
+ * operand images of both MLPs, copied into every CTA by the TMA engine) -- then ONE fused sm_100a kernel
+ * (shared by the two models of a conservative pair, CTAs partitioned by model): bilinear sampling
  * (P:334-337), endpoint MLP per block and colour MLP per texel on tcgen05 tensor cores
  * (P:257-272), endpoint quantization (R11-R13), palettes (Eq.7/8), per-texel
  * argmax of negative distance (Eq.9-10) and BC1/BC4 bit packing.
@@ -188,7 +190,9 @@ ntbc_status ntbc_debug_features(ntbc_model m, int width, int height, int row_beg
 
 /* Rows a5-a8 as a standalone kernel (quantize + palette + index + pack) fed fp32 MLP outputs in the
  * ntbc_debug_mlp layouts; same output convention as ntbc_decode_material.  fmts: host array of
- * n_textures formats (head order, R17).  Errors: NTBC_EINVAL, NTBC_ECUDA. */
+ * n_textures formats (head order, R17).  One thread per (block, texture), tiles staged by bulk copies when
+ * `colors` is 16-B aligned (any alignment accepted; out_blocks 8-B aligned).  Errors: NTBC_EINVAL,
+ * NTBC_ECUDA. */
 ntbc_status ntbc_pack(int n_textures, const int* fmts, const float* endpoints, const float* colors,
                       int width, int height, int row_begin, int row_end, void* const* out_blocks,
                       void* stream);

@@ -1,8 +1,10 @@
-// ntbc_kernels.cuh -- the three sm_100a kernels of the NTBC inference hot path:
-//   (1) fused_decode_kernel: grid dequant + multi-resolution bilinear sampling (rows a1-a2),
-//       endpoint and colour MLPs on tcgen05 tensor cores with TMEM accumulators (a3-a4),
-//       endpoint quantization, palettes, per-texel argmax, warp-ballot bit packing (a5-a8);
-//   (2) pack_kernel: rows a5-a8 standalone, fed fp32 MLP outputs (HBM-bound);
+// ntbc_kernels.cuh -- the sm_100a kernels of the NTBC inference hot path:
+//   (0) dequant_grids_kernel ("prep"): Eq.2 grid dequantization + the fused kernel's shared-memory prefix image;
+//   (1) fused_decode_kernel: multi-resolution bilinear sampling (rows a1-a2), endpoint and colour MLPs on
+//       tcgen05 tensor cores with TMEM accumulators (a3-a4; contract H or, SPLIT, contract F), endpoint
+//       quantization, palettes, per-texel argmax, bit packing (a5-a8);
+//   (2) pack_kernel_bt (default) / pack_kernel: rows a5-a8 standalone, fed fp32 MLP outputs (HBM-bound:
+//       0.7 of the measured bandwidth for pack_kernel_bt);
 //   (3) decode_bc_kernel: BC1/BC4 -> fp32 texels (row a9, verification).
 // Plus mma_probe_kernel (pins the tensor-core summation, R10).
 #pragma once

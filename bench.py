@@ -316,11 +316,12 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
     t_ms_max, k_ms_max = (float(x) for x in t_tensor.tolist())
 
-    # ---- contract F (binary32 activations, hi/lo split MMA operands) on the same material:
-    # the contract under which the decode meets north_star's rule literally against the plain definitions
-    contract_f = None
-    if world == 1:
-        ntbc.set_contract(models[0], 1)
+    # ---- the other arithmetic contracts on the same material (fused kernel only, timed like k_ms):
+    # F (binary32 activations, hi/lo split MMA operands) -- the contract under which the
+    # decode meets north_star's rule literally against the plain definitions; P (the hidden selu in binary16
+    # arithmetic on f16x2 lanes) -- faster, further from the plain definitions
+    def time_contract(c):
+        ntbc.set_contract(models[0], c)
         for _ in range(3):
             ntbc.decode_material([models[0]], W, H, outs=[out_all[0, k] for k in range(n_tex)], stream=stream)
         fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
@@ -335,9 +336,14 @@ def run_ours(args, rank, world, local_rank):
         ntbc.time_fused(None, None)
         ntbc.set_contract(models[0], 0)
         fk = sum(a.elapsed_time(b) for a, b in fev) / len(fev)
-        contract_f = {"kernel_ms": fk, "mblocks_per_s": plane * n_tex / (fk * 1e-3) / 1e6,
-                      "note": "fused kernel under ntbc_set_contract(m, 1); the headline value uses the paper's "
-                              "binary16 contract H"}
+        return {"kernel_ms": fk, "mblocks_per_s": plane * n_tex / (fk * 1e-3) / 1e6}
+
+    contract_f = contract_p = None
+    if world == 1:
+        contract_f = dict(time_contract(1), note="fused kernel under ntbc_set_contract(m, 1); the headline value "
+                                                 "uses the paper's binary16 contract H")
+        contract_p = dict(time_contract(2), note="fused kernel under ntbc_set_contract(m, 2): selu in binary16 "
+                                                 "arithmetic (~21% of activations not correctly rounded, §8.f2)")
 
     # ---- end to end through the C ABI with host buffers (pinned blob in, pinned BC words out), per rank
     model, blob = models[0], blobs[0]
@@ -426,7 +432,7 @@ def run_ours(args, rank, world, local_rank):
                    "ms_per_4k_material": t_ms_max * world / n_mat,
                    "latency_ms_per_4k_material": lat_ms if world > 1 else t_ms_max,
                    "contract": "H (binary16 MMA operands at every layer input, P:322)",
-                   "contract_f": contract_f},
+                   "contract_f": contract_f, "contract_p": contract_p},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": t_peak, "unit": "TFLOP/s",
                      "frac": achieved / t_peak, "traffic": traffic,
                      "kernel": "fused_decode_kernel", "kernel_ms": k_ms_max,

@@ -229,9 +229,13 @@ uint64_t ntbc_launch_count(void);
  * every layer input rounded to binary16, the paper's half-precision inference.
  * 1 = F: activations stay binary32 and each tcgen05 operand is the split hi = RN16(a), lo = RN16(a - hi),
  * multiplied by the same weights (2x the MMAs, half the work groups per SM) -- the contract under which the
- * decode meets north_star's agreement rule against the plain definitions literally.  Both are bit-exact
- * against the oracle's matching mode.  Applies to later decodes of the model (serialised with them).
- * Errors: NTBC_EINVAL (NULL, contract not 0/1, F for a naive model). */
+ * decode meets north_star's agreement rule against the plain definitions literally.  2 = P: as H, but the
+ * hidden selu is evaluated in binary16 ARITHMETIC on packed f16x2 lanes (DESIGN.md
+ * §8.f2: the most literal reading of P:322; faster, and ~21% of the activations one or more binary16 ulps
+ * from the correctly rounded selu).  All three are bit-exact against the oracle's matching mode.  Applies
+ * to later decodes of the model (serialised with them).  A conservative pair runs in one launch only when
+ * both models have the same contract.
+ * Errors: NTBC_EINVAL (NULL, contract not in {0, 1, 2}, F or P for a naive model). */
 ntbc_status ntbc_set_contract(ntbc_model m, int contract);
 
 /* Measurement hook (bench.py's roofline of the dominant kernel): while set, every fused-kernel launch

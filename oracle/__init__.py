@@ -81,6 +81,11 @@ def lib():
             "o_set_act_model": (None, [i32]),
             "o_get_act_model": (i32, []),
             "o_set_operand_model": (None, [i32]),
+            "o_f64_to_f16": (u16, [C.c_double]),
+            "o_h16_fma": (u16, [u16, u16, u16]),
+            "o_h16_mul": (u16, [u16, u16]),
+            "o_h16_sub": (u16, [u16, u16]),
+            "o_selu_half": (u16, [f32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -204,6 +209,20 @@ class contract_f:
 
     def __exit__(self, *exc):
         set_operand_model(0)
+        return False
+
+
+class contract_p:
+    """Context manager: the oracle computes contract P: the hidden selu in
+    binary16 arithmetic (R9-P, `o_selu_half`), everything else pinned as in contract H."""
+
+    def __enter__(self):
+        self._act = int(lib().o_get_act_model())
+        set_act_model(3)
+        return self
+
+    def __exit__(self, *exc):
+        set_act_model(self._act)
         return False
 
 

@@ -14,7 +14,9 @@
  * selu / sigmoid in float64 with libm and rounded once -- the reference the faithfulness tests
  * (tests/test_faithfulness.py) measure both the pinned oracle and the CUDA path against under
  * north_star's tolerance rule.  The binary16 operand rounding at every layer input
- * is part of the method and is the same in both modes.
+ * is part of the method and is the same in both modes.  Two more arithmetic contracts of the kernels
+ * have their own pinned modes: F (o_set_operand_model(1): binary32 activations, hi/lo split operands)
+ * and P (o_set_act_model(3): the selu in binary16 arithmetic, R9-P).
  *
  * Parity status per function: every function below is pinned by -m "not gpu"
  * tests.  o_dot's summation ORDER (R10: chunks of 16, window p = 25, round toward zero) is a
@@ -236,6 +238,7 @@ static float selu_neg_pinned(float z) {
 
 /* ------------------------------------------------------------------------- */
 /* activation model: 0 = the pinned op sequences above (R9, what the kernel computes);          */
+/* 3 = contract P (below: the selu in binary16 arithmetic, R9-P; the sigmoid stays pinned R9);   */
 /* 2 = the same in binary32 libm (expm1f / expf; a sensitivity variant, not a reference); */
 /* 1 = the PLAIN definitions (P:332-333 with the standard selu constants): evaluated in  */
 /* float64 with libm exp/expm1 and rounded once to binary32 -- the faithfulness reference.      */
@@ -247,21 +250,80 @@ static const double SELU_LAMBDA_D = 1.0507009873554804934, SELU_ALPHA_D = 1.6732
 
 static float selu_neg(float z) {
     if (g_act_plain == 2) return SELU_LA * expm1f(z);        /* a binary32 libm variant (sensitivity study) */
-    if (g_act_plain) return (float)(SELU_LAMBDA_D * SELU_ALPHA_D * expm1((double)z));
+    if (g_act_plain == 1) return (float)(SELU_LAMBDA_D * SELU_ALPHA_D * expm1((double)z));
     return selu_neg_pinned(z);
 }
 float o_expm1(float x) { return selu_neg_pinned(x) / SELU_LA; }   /* for the accuracy pin only (x <= 0) */
 
+/* ------------------------------------------------------------------------- */
+/* contract P (R9-P): the selu evaluated in IEEE binary16 arithmetic,    */
+/* the most literal reading of "inference is executed in the half-precision floating points". */
+/* Every step is ONE binary16 operation: the exact result (computed exactly in binary64 -- a product   */
+/* of two binary16 values has 22 bits, and a binary16 fma's exact result is either representable in   */
+/* binary64 or, when it is not, lies farther than 2^-53 |x| from every binary16 rounding midpoint, so  */
+/* the binary64 fma followed by one binary16 rounding equals the single rounding; pinned against      */
+/* exact rational arithmetic by test_h16_ops_are_single_roundings) rounded once to nearest-even.      */
+/* ------------------------------------------------------------------------- */
+uint16_t o_f64_to_f16(double x) {
+    uint64_t u; memcpy(&u, &x, 8);
+    uint16_t sign = (uint16_t)((u >> 48) & 0x8000);
+    double a = fabs(x);
+    if (a != a) return (uint16_t)(sign | 0x7e00);
+    if (a >= 65520.0) return (uint16_t)(sign | 0x7c00);       /* rounds to inf */
+    if (a == 0.0) return sign;
+    int E; (void)frexp(a, &E);                                /* a = fr * 2^E, fr in [0.5,1) */
+    int qexp = (E - 1 >= -14) ? (E - 1 - 10) : -24;           /* the binary16 quantum of a's binade */
+    double scaled = ldexp(a, -qexp);                          /* exact (a power-of-two scaling) */
+    double fl = floor(scaled), rem = scaled - fl;             /* rem exact: fl and scaled share the binade */
+    uint32_t mant = (uint32_t)fl;
+    if (rem > 0.5 || (rem == 0.5 && (mant & 1))) mant++;      /* round half to even */
+    if (qexp == -24) return (uint16_t)(sign | mant);
+    int bexp = qexp + 25;
+    if (mant == 2048) { mant = 1024; bexp++; }
+    if (bexp >= 31) return (uint16_t)(sign | 0x7c00);
+    return (uint16_t)(sign | (bexp << 10) | (mant - 1024));
+}
+static double h2d(uint16_t h) { return (double)o_f16_to_f32(h); }
+uint16_t o_h16_fma(uint16_t a, uint16_t b, uint16_t c) { return o_f64_to_f16(fma(h2d(a), h2d(b), h2d(c))); }
+uint16_t o_h16_mul(uint16_t a, uint16_t b) { return o_f64_to_f16(h2d(a) * h2d(b)); }
+uint16_t o_h16_sub(uint16_t a, uint16_t b) { return o_f64_to_f16(h2d(a) - h2d(b)); }
+
+/* R9-P, step by step (the constants are binary16 bit patterns):
+   h = RN16(z); z's sign decides (h = -0 takes the negative branch, which gives +0 there);
+   positive: RN16(lambda16 h), lambda16 = RN16(1.0507...) = 0x3C34;
+   negative: x = max(h, -10) (below -10, lambda alpha e^x is under a quarter ulp of lambda alpha16);
+     t = RN16(x log2e16 + 1039), an integer in [1025, 1039] (the binary16 quantum is 1 there), n = t - 1039;
+     g = RN16(x - n ln2hi), ln2hi = 0.693359375 (exact: Cody-Waite); g = RN16(g - n ln2lo16);
+     P = RN16(RN16(C2 g + C1) g + C0), u = RN16(g RN16(g P) + g)  -- u ~ e^g - 1 on |g| <= 0.37;
+     S = lambda alpha16 2^n (exact: the binary16 exponent field of 0x3F08 lowered by -n, n >= -14);
+     neg = RN16(S u + RN16(S - lambda alpha16)). */
+uint16_t o_selu_half(float z) {
+    const uint16_t h = o_f32_to_f16(z);
+    if (!(h & 0x8000)) return o_h16_mul(h, 0x3C34);
+    const uint16_t x = h2d(h) > -10.0 ? h : 0xC900;           /* max(h, -10); h = -0 stays -0 */
+    const uint16_t t = o_h16_fma(x, 0x3DC5, 0x640F);
+    const uint16_t nf = o_h16_sub(t, 0x640F);
+    uint16_t g = o_h16_fma(nf, 0xB98C, x);
+    g = o_h16_fma(nf, 0x0AF4, g);
+    uint16_t P = o_h16_fma(0x295B, g, 0x315B);
+    P = o_h16_fma(P, g, 0x3800);
+    const uint16_t u = o_h16_fma(g, o_h16_mul(g, P), g);
+    const int n = (int)h2d(nf);                                /* exact integer in [-14, 0] */
+    const uint16_t S = (uint16_t)(0x3F08 + (n << 10));         /* lambda alpha16 * 2^n, a normal binary16 */
+    return o_h16_fma(S, u, o_h16_sub(S, 0x3F08));
+}
+
 /* selu ([selu] Klambauer et al.): lambda z (z > 0) else lambda alpha (e^z - 1) */
 float o_selu(float z) {
+    if (g_act_plain == 3) return o_f16_to_f32(o_selu_half(z));
     if (g_act_plain == 2) return z > 0.0f ? SELU_L * z : selu_neg(z);
-    if (g_act_plain) return z > 0.0f ? (float)(SELU_LAMBDA_D * (double)z) : selu_neg(z);
+    if (g_act_plain == 1) return z > 0.0f ? (float)(SELU_LAMBDA_D * (double)z) : selu_neg(z);
     return z > 0.0f ? SELU_L * z : selu_neg(z);
 }
 /* sigmoid: 1 / (1 + e^-z), IEEE division */
 float o_sigmoid(float z) {
     if (g_act_plain == 2) return 1.0f / (1.0f + expf(-z));
-    if (g_act_plain) return (float)(1.0 / (1.0 + exp(-(double)z)));
+    if (g_act_plain == 1) return (float)(1.0 / (1.0 + exp(-(double)z)));
     float d = 1.0f + o_exp(-z); return 1.0f / d;
 }
 

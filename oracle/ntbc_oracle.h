@@ -41,9 +41,17 @@ float    o_exp(float x);                                       /* pinned E, R9 *
 float    o_expm1(float x);                                     /* selu_neg(x)/(lambda alpha), accuracy pin only */
 float    o_selu(float z);                                      /* P:333, R8 */
 float    o_sigmoid(float z);                                   /* P:332, R8 */
-/* activation model: 0 = pinned op sequences (R9, default), 1 = plain float64/libm definitions */
+/* activation model: 0 = pinned op sequences (R9, default), 1 = plain float64/libm definitions,
+   2 = binary32 libm (sensitivity variant), 3 = contract P: selu in binary16 arithmetic (R9-P) */
 void     o_set_act_model(int plain);
 int      o_get_act_model(void);
+/* IEEE binary16 arithmetic (contract P): each op is the exact result rounded once to
+   binary16, nearest-even */
+uint16_t o_f64_to_f16(double x);                               /* RN-even, directly from binary64 */
+uint16_t o_h16_fma(uint16_t a, uint16_t b, uint16_t c);
+uint16_t o_h16_mul(uint16_t a, uint16_t b);
+uint16_t o_h16_sub(uint16_t a, uint16_t b);
+uint16_t o_selu_half(float z);                                 /* R9-P, the contract-P hidden activation */
 
 /* Summation model of one layer's dot product (R10).
    mode 0 = CR  : b + sum_k w_k a_k exactly, one RN to fp32.

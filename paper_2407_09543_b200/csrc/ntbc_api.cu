@@ -179,7 +179,8 @@ struct ntbc_model_s {
   // decodes of one model on different streams are ordered on the device by `last_done`, recorded after
   // each launch (they share the model's fp32 grid region, rewritten by every decode's dequant launch)
   std::recursive_mutex mu;
-  int contract = 0;            // MMA operand contract: 0 = H (binary16 activations), 1 = F
+  int contract = 0;            // arithmetic contract: 0 = H (binary16 activations), 1 = F,
+                               // 2 = P (binary16 selu arithmetic)
   cudaEvent_t last_done = nullptr;
   cudaStream_t last_stream = nullptr;
   uint8_t* d_blob = nullptr;   // weight slot: the blob, then at fg_base its grids dequantized to fp32
@@ -284,8 +285,10 @@ struct DevGuard {
 
 template <int H, int NWG, bool DUMP, bool SPLIT = false>
 ntbc_status launch_fused_t(const FusedLaunch& L, size_t smem, int grid, cudaStream_t st) {
-  auto kern = SPLIT ? fused_decode_kernel<H, NWG, DUMP, false, true>
-                    : L.m[0].naive ? fused_decode_kernel<H, NWG, DUMP, true> : fused_decode_kernel<H, NWG, DUMP, false>;
+  auto kern = SPLIT          ? fused_decode_kernel<H, NWG, DUMP, false, true>
+              : L.m[0].naive ? fused_decode_kernel<H, NWG, DUMP, true>
+              : L.m[0].half  ? fused_decode_kernel<H, NWG, DUMP, false, false, true>   // contract P
+                             : fused_decode_kernel<H, NWG, DUMP, false>;
   CUDA_TRY(allow_smem((const void*)kern, 227 * 1024));
   if (!DUMP && g_time_fused[0]) CUDA_TRY(cudaEventRecord(g_time_fused[0], st));
   kern<<<grid, NWG * 128, smem, st>>>(L);
@@ -376,7 +379,8 @@ ntbc_status prepare_fused(ntbc_model_s* m, FusedParams& p, bool dump, cudaStream
   p.units_per_row = (p.BW + kUnitBlocks - 1) / kUnitBlocks;
   p.n_units = p.units_per_row * (p.row_end - p.row_begin);
   const int maxo = a.dims[0][4] > a.dims[1][4] ? a.dims[0][4] : a.dims[1][4];
-  p.split = m->contract;
+  p.split = m->contract == 1;
+  p.half = m->contract == 2;
   const uint32_t a_kmajor = 128u * a.hidden * 2u * (p.split ? 2u : 1u);   // F: hi and lo chunks
   const uint32_t a_stage = 128u * 4u * (uint32_t)((maxo + 1) & ~1);      // fp32 staging [ch][128], pairs
   p.a_bytes = (uint32_t)((std::max(a_kmajor, a_stage) + 127) & ~127u);
@@ -1174,8 +1178,8 @@ uint64_t ntbc_launch_count(void) { return g_launches.load(); }
 
 ntbc_status ntbc_set_contract(ntbc_model m, int contract) {
   if (!m) return fail(NTBC_EINVAL, "model is NULL");
-  if (contract != 0 && contract != 1) return fail(NTBC_EINVAL, "contract %d not in {0 (H), 1 (F)}", contract);
-  if (contract == 1 && m->arch.naive) return fail(NTBC_EINVAL, "contract F is not provided for the naive variant");
+  if (contract < 0 || contract > 2) return fail(NTBC_EINVAL, "contract %d not in {0 (H), 1 (F), 2 (P)}", contract);
+  if (contract != 0 && m->arch.naive) return fail(NTBC_EINVAL, "contracts F and P are not provided for the naive variant");
   std::lock_guard<std::recursive_mutex> lk(m->mu);
   m->contract = contract;
   return NTBC_OK;

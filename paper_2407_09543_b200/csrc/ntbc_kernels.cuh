@@ -1,7 +1,7 @@
 // ntbc_kernels.cuh -- the sm_100a kernels of the NTBC inference hot path:
 //   (0) dequant_grids_kernel ("prep"): Eq.2 grid dequantization + the fused kernel's shared-memory prefix image;
 //   (1) fused_decode_kernel: multi-resolution bilinear sampling (rows a1-a2), endpoint and colour MLPs on
-//       tcgen05 tensor cores with TMEM accumulators (a3-a4; contract H or, SPLIT, contract F), endpoint
+//       tcgen05 tensor cores with TMEM accumulators (a3-a4; contract H, SPLIT contract F or HALF contract P), endpoint
 //       quantization, palettes, per-texel argmax, bit packing (a5-a8);
 //   (2) pack_kernel_bt (default) / pack_kernel: rows a5-a8 standalone, fed fp32 MLP outputs (HBM-bound:
 //       0.7 of the measured bandwidth for pack_kernel_bt);
@@ -111,6 +111,7 @@ struct FusedParams {
   int vec16;                    // every out pointer 16-B aligned and BW even: a warp's two adjacent blocks'
                                 // words leave as one 16-byte store (else one 8-byte store per block)
   int split;                    // contract F (host side; the kernel's SPLIT template parameter follows it)
+  int half;                     // contract P: binary16 selu arithmetic (host side; template parameter HALF)
   int n_bc1, n_bc4;             // the texture indices of each format, in head order
   int tex_bc1[kMaxTex], tex_bc4[kMaxTex];
 };
@@ -285,7 +286,7 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, in
 // (128 blocks) then up to 16 colour tiles (8 blocks = 128 texels).  More independent groups per SM
 // hide more of the dependent epilogue latency.  Units are claimed from a global
 // counter (dynamic scheduling) so they finish in row order (pipelined copy-back, ntbc_api.cu).
-template <int H, int NWG, bool DUMP, bool NAIVE, bool SPLIT = false>
+template <int H, int NWG, bool DUMP, bool NAIVE, bool SPLIT = false, bool HALF = false>
 __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid_constant__ FusedLaunch L) {
   constexpr int KA = SPLIT ? 2 * H : H;   // K width (fp16 columns) of the A operand rows
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -421,7 +422,8 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
         uint32_t hv[4];
 #pragma unroll
         for (int j = 0; j < 4; j++)
-          hv[j] = selu2_h2(__uint_as_float(b8[c & 1][2 * j]), __uint_as_float(b8[c & 1][2 * j + 1]));
+          hv[j] = HALF ? selu2_h16(__uint_as_float(b8[c & 1][2 * j]), __uint_as_float(b8[c & 1][2 * j + 1]))
+                       : selu2_h2(__uint_as_float(b8[c & 1][2 * j]), __uint_as_float(b8[c & 1][2 * j + 1]));
         *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 8, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
         if (c + 1 < H / 8) tmem_wait_ld8(b8[(c + 1) & 1]);
       }
@@ -450,7 +452,8 @@ __global__ void __launch_bounds__(NWG * 128, 1) fused_decode_kernel(const __grid
       } else {
 #pragma unroll
         for (int j = 0; j < 8; j++)
-          hv[j] = selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
+          hv[j] = HALF ? selu2_h16(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]))
+                       : selu2_h2(__uint_as_float(buf[c & 1][2 * j]), __uint_as_float(buf[c & 1][2 * j + 1]));
         *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 16, H)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
         *reinterpret_cast<uint4*>(As + kmajor_offset(r, c * 16 + 8, H)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
       }

@@ -322,5 +322,6 @@ def time_fused(start_event=None, end_event=None):
 
 
 def set_contract(model, contract: int):
-    """ntbc_set_contract: 0 = H (binary16 activations, the paper's), 1 = F (binary32 activations, hi/lo operands)."""
+    """ntbc_set_contract: 0 = H (binary16 activations, the paper's), 1 = F (binary32 activations, hi/lo operands),
+    2 = P (H with the selu evaluated in binary16 arithmetic on f16x2 lanes)."""
     _check(_lib.ntbc_set_contract(model._h, int(contract)))

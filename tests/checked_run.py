@@ -84,6 +84,21 @@ def main():
         for k in range(m.n_tex):
             assert np.array_equal(u64(outs[k]), ref[k]), ("contract F", w, hh, k)
             h.update(u64(outs[k]).tobytes())
+    # contract P (binary16 selu arithmetic) on seeded random non-naive models, vs the oracle's P mode
+    n_p = 0
+    for blob, w, hh, r0, r1, misalign in fuzz_cases(40, seed=93):
+        om = oracle.Model(blob)
+        if om.naive or n_p >= 6:
+            continue
+        n_p += 1
+        m = ntbc.Model(blob)
+        ntbc.set_contract(m, 2)
+        outs = ntbc.decode_material([m], w, hh, row_begin=r0, row_end=r1)
+        with oracle.contract_p():
+            ref = om.decode_material(w, hh, r0, r1)
+        for k in range(m.n_tex):
+            assert np.array_equal(u64(outs[k]), ref[k]), ("contract P", w, hh, k)
+            h.update(u64(outs[k]).tobytes())
     # conservative pair (one launch, CTAs partitioned by model)
     rgb = synth.serialize(synth.random_model(synth.ModelSpec([synth.BC1, synth.BC1], block_levels=4, texel_levels=5), 5))
     sc = synth.serialize(synth.random_model(synth.ModelSpec([synth.BC4] * 4, block_levels=4, texel_levels=5), 6))

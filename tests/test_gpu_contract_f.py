@@ -105,7 +105,7 @@ def test_contract_f_meets_the_literal_rule_vs_plain(ntbc, cfg, rows):
 def test_contract_f_api(ntbc):
     m = ntbc.Model(synth.model_blob(1))
     with pytest.raises(ntbc.NtbcError):
-        ntbc.set_contract(m, 2)
+        ntbc.set_contract(m, 3)
     naive = ntbc.Model(synth.model_blob(8))
     with pytest.raises(ntbc.NtbcError):
         ntbc.set_contract(naive, 1)

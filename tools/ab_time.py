@@ -17,6 +17,8 @@ from paper_2407_09543_b200 import ntbc
 cfg, reps = int(sys.argv[1]), int(sys.argv[2])
 W, H, _ = synth.config_shape(cfg)
 m = ntbc.Model(synth.model_blob(cfg))
+if os.environ.get("NTBC_CONTRACT"):
+    ntbc.set_contract(m, int(os.environ["NTBC_CONTRACT"]))
 outs = ntbc.alloc_outputs([m], W, H)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 s = torch.cuda.current_stream()
@@ -29,7 +31,8 @@ for _ in range(reps):
     a.record(s); ntbc.decode_material([m], W, H, outs=outs, stream=s); b.record(s)
     torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
 ts.sort()
-print(json.dumps({"lib": os.environ.get("NTBC_LIB", "libntbc.so"), "nwg": os.environ.get("NTBC_NWG"), "cfg": cfg, "median_ms": ts[len(ts) // 2],
+print(json.dumps({"lib": os.environ.get("NTBC_LIB", "libntbc.so"), "nwg": os.environ.get("NTBC_NWG"),
+                  "contract": os.environ.get("NTBC_CONTRACT", "0"), "cfg": cfg, "median_ms": ts[len(ts) // 2],
                   "min_ms": ts[0]}))
 """ % ROOT
 

@@ -2,6 +2,8 @@
 // SMSP with many independent chains (what bounds the hidden-layer epilogue).
 #include <cstdio>
 #include <cstdint>
+#include <utility>
+#include <cuda_fp16.h>
 #include "../../paper_2407_09543_b200/csrc/bc_device.cuh"
 #define CH 8
 #define ITERS 1024
@@ -66,6 +68,37 @@ __device__ __forceinline__ uint32_t selu_mufu(float z0, float z1) {
   asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(h) : "r"(hn), "r"(hp), "r"(m));
   return h;
 }
+
+// V = 5: the whole selu in binary16 arithmetic on packed f16x2 lanes:
+// h = RN16(z); pos = RN16(lambda16 h); x = max(h, -10); n = rint(x log2e) via the 1039 magic (ulp 1 in
+// [1024, 2048)); g = x - n ln2 (Cody-Waite: the hi product and difference are exact in binary16, then the lo
+// term); e^g - 1 = g + g (g P(g)) with a degree-2 P; S = lambda alpha16 2^n by exponent insertion from t's
+// mantissa bits; neg = fma(S, u, S - lambda alpha16); select by h's sign.  11 FMA-pipe + 6 ALU instructions.
+__device__ __forceinline__ uint32_t hf2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d; asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d; }
+__device__ __forceinline__ uint32_t hm2(uint32_t a, uint32_t b) {
+  uint32_t d; asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t hs2(uint32_t a, uint32_t b) {
+  uint32_t d; asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+template <bool LO>
+__device__ __forceinline__ uint32_t selu_h16(float z0, float z1) {
+  uint32_t h, x, m, r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(z1), "f"(z0));
+  const uint32_t pos = hm2(h, 0x3C343C34u);
+  asm("max.f16x2 %0, %1, %2;" : "=r"(x) : "r"(h), "r"(0xC900C900u));
+  const uint32_t t = hf2(x, 0x3DC53DC5u, 0x640F640Fu);
+  const uint32_t nf = hs2(t, 0x640F640Fu);
+  uint32_t g = hf2(nf, 0xB98CB98Cu, x);
+  if (LO) g = hf2(nf, 0x0AF40AF4u, g);
+  uint32_t P = hf2(0x295B295Bu, g, 0x315B315Bu);
+  P = hf2(P, g, 0x38003800u);
+  const uint32_t u = hf2(g, hm2(g, P), g);
+  const uint32_t S = ((t & 0x000F000Fu) << 10) + 0x03080308u;
+  const uint32_t neg = hf2(S, u, hs2(S, 0x3F083F08u));
+  asm("prmt.b32 %0, %1, %2, 0xBB99;" : "=r"(m) : "r"(h), "r"(0u));
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(neg), "r"(pos), "r"(m));
+  return r;
+}
 template <int V>
 __global__ void k(float* out, int seed, long long* cyc) {
   float a[CH], b[CH];
@@ -77,7 +110,8 @@ __global__ void k(float* out, int seed, long long* cyc) {
   for (int it = 0; it < ITERS; it++) {
 #pragma unroll
     for (int i = 0; i < CH; i++) {
-      uint32_t s = V == 9 ? selu2_h2(a[i], b[i]) : V == 4 ? selu_mufu(a[i], b[i]) : selu_v<V>(a[i], b[i]);
+      uint32_t s = V == 9 ? selu2_h2(a[i], b[i]) : V == 4 ? selu_mufu(a[i], b[i]) : V == 5 ? selu_h16<true>(a[i], b[i])
+                   : V == 6 ? selu_h16<false>(a[i], b[i]) : selu_v<V>(a[i], b[i]);
       h[i] ^= s;
       a[i] = __uint_as_float(__float_as_uint(a[i]) ^ (s & 0x10u));   // data dependence (ALU ops)
       b[i] = __uint_as_float(__float_as_uint(b[i]) ^ (s & 0x100000u));
@@ -107,12 +141,47 @@ __global__ void ex2_int_check(int* bad) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(q) : "f"(-(float)(-n)));
   if (__float_as_uint(q) != __float_as_uint(want)) atomicAdd(bad + 1, 1);
 }
+
+// accuracy against the correctly rounded binary16 selu (float64 expm1 on the device, then RN16)
+template <int V>
+__global__ void acc_k(int n, float lo, float hi, unsigned long long* bad, int* maxd) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * i + 1 >= n) return;
+  const float z0 = lo + (hi - lo) * (2 * i) / n, z1 = lo + (hi - lo) * (2 * i + 1) / n;
+  const uint32_t g = V == 9 ? selu2_h2(z0, z1) : selu_h16<V == 5>(z0, z1);
+  const float zz[2] = {z0, z1};
+  for (int k = 0; k < 2; k++) {
+    const double z = zz[k];
+    const double s = z > 0 ? 1.0507009873554804934 * z : 1.0507009873554804934 * 1.6732632423543772848 * expm1(z);
+    const __half ref = __double2half(s);
+    const short a = (short)((g >> (16 * k)) & 0xFFFF), b = (short)__half_as_ushort(ref);
+    if (a != b) {
+      atomicAdd(bad, 1ull);
+      const int ia = a < 0 ? -(a & 0x7FFF) : a, ib = b < 0 ? -(b & 0x7FFF) : b;
+      atomicMax(maxd, abs(ia - ib));
+    }
+  }
+}
+template <int V>
+void acc(const char* name) {
+  unsigned long long* bad; int* md; cudaMallocManaged(&bad, 8); cudaMallocManaged(&md, 4);
+  const int n = 1 << 24;
+  for (auto rg : {std::pair<float, float>{-12.f, 0.f}, std::pair<float, float>{-0.05f, 0.f}, std::pair<float, float>{0.f, 8.f}}) {
+    *bad = 0; *md = 0;
+    acc_k<V><<<n / 2 / 256, 256>>>(n, rg.first, rg.second, bad, md); cudaDeviceSynchronize();
+    printf("%-34s z in [%g, %g]: %.4f%% not correctly rounded, max %d binary16 ulp\n", name, rg.first, rg.second,
+           100.0 * *bad / n, *md);
+  }
+  cudaFree(bad); cudaFree(md);
+}
 int main() {
+  acc<9>("selu2_h2 (v4, binary32)"); acc<5>("binary16 f16x2 selu"); acc<6>("binary16, no ln2_lo term");
   { int* b; cudaMallocManaged(&b, 8); b[0] = b[1] = 0; ex2_int_check<<<1, 256>>>(b); cudaDeviceSynchronize();
     printf("ex2.approx.ftz of integers -200..55: %d / %d mismatches vs exact 2^n (0 below 2^-126)\n", b[0], b[1]); }
   for (int w : {16, 32}) {
     run<9>("selu2_h2 (library)", w); run<0>("v4 copy", w); run<1>("no clamp", w); run<2>("neg only (no select/pos)", w);
     run<3>("degree 3", w); run<4>("MUFU 2^n, no clamp", w);
+    run<5>("binary16 f16x2 selu", w); run<6>("binary16, no ln2_lo term", w);
   }
   return 0;
 }

@@ -15,6 +15,8 @@ def main():
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     W, H, _ = synth.config_shape(cfg)
     m = ntbc.Model(synth.model_blob(cfg))
+    if os.environ.get("NTBC_CONTRACT"):   # 1 = F, 2 = P
+        ntbc.set_contract(m, int(os.environ["NTBC_CONTRACT"]))
     outs = ntbc.alloc_outputs([m], W, H)
     for _ in range(reps):
         ntbc.decode_material([m], W, H, outs=outs)

@@ -3,13 +3,14 @@
 The material is MetalPlates013-shaped: six 4096^2 textures, 2 BC1 (diffuse, normal) + 4 BC4
 (displacement, roughness, AO, metalness).  Workloads:
   CS BC1&BC4  -- conservative: an all-BC1 model (2 textures) and an all-BC4 model (4 textures),
-                 one ntbc_decode_material call with both (two persistent launches back to back);
+                 one ntbc_decode_material call with both (ONE persistent launch, CTAs partitioned by model);
   CS BC1 only -- the RGB model alone;
   AG BC1&BC4  -- aggressive: one model with all 6 textures (config 6, C3');
   AG BC1 only -- an aggressive model over the two RGB textures only.
 Random-init weights of the paper architecture (seeded), synthetic grids; kernel time by CUDA events
 on the launching stream, L2 flushed (256 MiB write) between steps outside the events.  Writes
-profiles/tab1_<tag>.json and prints a table with the paper's RX 7900 XT times beside ours.
+profiles/tab1_<tag>.json and prints a table with the paper's RX 7900 XT times beside ours.  Env
+NTBC_CONTRACT=2 runs every model under contract P (binary16 selu arithmetic).
 
 usage: python tools/tab1.py [tag] [steps]
 """
@@ -25,6 +26,7 @@ import synth  # noqa: E402
 from paper_2407_09543_b200 import ntbc  # noqa: E402
 
 W = H = 4096
+CONTRACT = int(os.environ.get("NTBC_CONTRACT", "0"))
 PAPER_MS = {"CS BC1&BC4": 49.84, "CS BC1 only": 25.57, "AG BC1&BC4": 27.31, "AG BC1 only": 25.96}
 
 
@@ -42,6 +44,8 @@ def models_for(workload):
 
 def time_workload(blobs, steps):
     models = [ntbc.Model(b) for b in blobs]
+    for m in models:
+        ntbc.set_contract(m, CONTRACT)
     outs = ntbc.alloc_outputs(models, W, H)
     stream = torch.cuda.Stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -69,6 +73,7 @@ def main(tag="r01", steps=20):
         rows.append({"workload": wl, "textures": n_tex, "ms": ms, "mblocks_per_s": blocks / ms / 1e3,
                      "paper_ms_rx7900xt": PAPER_MS[wl], "speedup_vs_paper": PAPER_MS[wl] / ms})
     out = {"tag": tag, "gpu": torch.cuda.get_device_name(0), "width": W, "height": H, "steps": steps,
+           "contract": {0: "H", 1: "F", 2: "P"}[CONTRACT],
            "timing": "CUDA events, kernel only, L2 flushed between steps", "rows": rows}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"tab1_{tag}.json"), "w") as f:

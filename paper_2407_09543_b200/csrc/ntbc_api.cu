@@ -496,9 +496,12 @@ typedef CUresult (*dev_get_fn)(CUdevice*, int);
 wait64_fn g_wait64 = nullptr;
 
 bool stream_waits_supported(int device) {
-  static int cached[64];  // 0 unknown, 1 yes, 2 no
+  static std::atomic<int> cached[64];  // 0 unknown, 1 yes, 2 no (several host threads may probe at once)
+  static std::mutex probe_mu;
   if (device < 0 || device >= 64) return false;
-  if (cached[device]) return cached[device] == 1;
+  if (cached[device].load()) return cached[device].load() == 1;
+  std::lock_guard<std::mutex> lk(probe_mu);
+  if (cached[device].load()) return cached[device].load() == 1;
   if (const char* e = getenv("NTBC_NO_PIPELINED_COPY")) if (atoi(e)) { cached[device] = 2; return false; }
   void *w = nullptr, *ga = nullptr, *gd = nullptr;
   cudaDriverEntryPointQueryResult q1, q2, q3;
@@ -543,10 +546,25 @@ bool ensure_copy_state(ntbc_model_s* m) {
             cudaMalloc(&m->d_progress, kMaxChunks * sizeof(unsigned long long)) == cudaSuccess &&
             cudaMemset(m->d_progress, 0, kMaxChunks * sizeof(unsigned long long)) == cudaSuccess &&
             cudaDeviceSynchronize() == cudaSuccess;
-  if (!ok) {
+  if (!ok) {   // release what was created, so a later call starts from scratch (no leaks on retry)
     cudaGetLastError();
     cudaFree(m->d_progress);
     m->d_progress = nullptr;
+    cudaFree(m->slot_blob[1]);
+    m->slot_blob[1] = nullptr;
+    for (int i = 0; i < kCopyStreams; i++) {
+      if (m->copy_stream[i]) cudaStreamDestroy(m->copy_stream[i]);
+      if (m->copy_done[i]) cudaEventDestroy(m->copy_done[i]);
+      m->copy_stream[i] = nullptr;
+      m->copy_done[i] = nullptr;
+    }
+    for (cudaEvent_t* e : {&m->copy_start, &m->uploaded, &m->slot_free[0], &m->slot_free[1]}) {
+      if (*e) cudaEventDestroy(*e);
+      *e = nullptr;
+    }
+    if (m->upload_stream) cudaStreamDestroy(m->upload_stream);
+    m->upload_stream = nullptr;
+    cudaGetLastError();
     return false;
   }
   m->slot_blob[0] = m->d_blob;
@@ -637,6 +655,7 @@ ntbc_status ntbc_model_upload_async(ntbc_model m, const void* blob, size_t nbyte
 
 ntbc_status ntbc_model_get_info(ntbc_model m, ntbc_model_info* out) {
   if (!m || !out) return fail(NTBC_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> lk(m->mu);   // slot and scratch sizes change under host-path calls
   const Arch& a = m->arch;
   memset(out, 0, sizeof *out);
   out->n_textures = a.n_tex;

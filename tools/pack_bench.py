@@ -53,8 +53,9 @@ def main(tag="r01", steps=20):
            "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)",
            "words_equal_fused_kernel": same,
-           "bound_note": "SIMT issue (ALU pipe ~61%, 71% issue-active), not HBM: ncu DRAM bytes = the algorithmic "
-                         "bytes (profiles/r01zd_pack_ncu.md), so frac is HBM headroom, not the limiting resource"}
+           "bound_note": "ncu DRAM bytes = the algorithmic bytes (fp32 MLP outputs read once + the BC words written "
+                         "once; profiles/r02ev_pack_ncu.md); ALU pipe ~58%, 67% issue-active: the remaining "
+                         "headroom to the copy bandwidth is SIMT issue (DESIGN.md §7.2)"}
     print(json.dumps(out))
     with open(os.path.join(ROOT, "profiles", f"pack_{tag}.json"), "w") as f:
         json.dump(out, f, indent=1)

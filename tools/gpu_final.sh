@@ -22,7 +22,14 @@ NTBC_CONTRACT=2 timeout 900 ncu --set full --clock-control none --import-source 
   python tools/profile_step.py 3 2 > gpurun_out/${tag}_ncu_full_p.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:pack_kernel -c 1 -o gpurun_out/${tag}_pack \
   python tools/pack_bench.py ${tag} 2 > gpurun_out/${tag}_ncu_pack.log 2>&1
+# summaries on the box (gpurun copies back at most 64 MiB): contract P first, then H (latest_fused_traffic.json = H)
+python tools/ncu_summary.py gpurun_out/${tag}_p.ncu-rep ${tag}_p > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/${tag}.ncu-rep ${tag} > /dev/null 2>&1
+cp profiles/${tag}_p_fused_ncu.* profiles/${tag}_fused_ncu.* profiles/latest_fused_traffic.json gpurun_out/ 2>/dev/null
+ncu -i gpurun_out/${tag}_pack.ncu-rep --page raw --csv > gpurun_out/${tag}_pack_raw.csv 2>/dev/null
+python tools/ncu_lines.py gpurun_out/${tag}.ncu-rep 16777216 60 > gpurun_out/${tag}_lines.txt 2>/dev/null
+mv gpurun_out/${tag}_p.ncu-rep gpurun_out/${tag}_pack.ncu-rep /tmp/ 2>/dev/null
 python tools/tab1.py ${tag} 20 > gpurun_out/${tag}_tab1.log 2>&1; cp profiles/tab1_${tag}.json gpurun_out/
 NTBC_CONTRACT=2 python tools/tab1.py ${tag}_p 20 > gpurun_out/${tag}_tab1_p.log 2>&1; cp profiles/tab1_${tag}_p.json gpurun_out/
 python tools/pack_bench.py ${tag} 20 > gpurun_out/${tag}_pack.log 2>&1; cp profiles/pack_${tag}.json gpurun_out/
-ls -la gpurun_out | tail -5
+du -sh gpurun_out; ls -la gpurun_out | tail -5

@@ -309,7 +309,7 @@ uint16_t o_selu_half(float z) {
     P = o_h16_fma(P, g, 0x3800);
     const uint16_t u = o_h16_fma(g, o_h16_mul(g, P), g);
     const int n = (int)h2d(nf);                                /* exact integer in [-14, 0] */
-    const uint16_t S = (uint16_t)(0x3F08 + (n << 10));         /* lambda alpha16 * 2^n, a normal binary16 */
+    const uint16_t S = (uint16_t)(0x3F08 + n * 1024);          /* lambda alpha16 * 2^n, a normal binary16 */
     return o_h16_fma(S, u, o_h16_sub(S, 0x3F08));
 }
 

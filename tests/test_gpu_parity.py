@@ -188,6 +188,15 @@ def test_ragged_and_degenerate_shapes(ntbc, W, H):
     check_material(ntbc, blob, W, H, [(0, H // 4)])
 
 
+@pytest.mark.parametrize("W,H,rows", [(16384, 16, [(0, 4)]),                        # 32 units per block row
+                                      (16, 16384, [(0, 1), (2047, 2048), (4095, 4096)]),   # 1 partial unit per row
+                                      (8192, 8192, [(0, 1), (1024, 1025), (2047, 2048)])])  # 2x the 4k side
+def test_large_and_extreme_aspect_shapes(ntbc, W, H, rows):
+    """Sizes beyond the 4k configs with the C3 architecture (paper grids): the widest and tallest block-row
+    layouts and an 8192^2 material (67 M texels), decoded in one launch, rows compared with the oracle."""
+    check_material(ntbc, 3, W, H, rows)
+
+
 def test_closed_form_model(ntbc):
     big = 65504.0
     sp = synth.ModelSpec([synth.BC1, synth.BC4], hidden=16, block_levels=2, block_coarsest=8, texel_levels=2,

@@ -204,18 +204,27 @@ def test_mlp_single_layer_vs_torch_float64():
 
 
 def test_mlp_paper_architecture_vs_torch_float64():
-    """14/16 -> 64 -> 64 -> 64 -> N with selu/sigmoid.  fp16 re-rounding of hidden
-    activations may flip by one binary16 ulp between the two evaluations, so the bound is loose;
-    a transposed weight, a dropped bias or a wrong activation is off by >> 1e-2."""
+    """16 -> 64 -> 64 -> 64 -> 9 with selu/sigmoid against torch float64 with binary16 layer
+    inputs.  The plain-definition mode agrees to 1e-6 relative on every sample (it differs from torch only
+    by its binary32 roundings): this pins the architecture, the operand rounding, the weight orientation and
+    the selu constants tightly.  The pinned mode (R9, R10) agrees to 1e-5 on at least 90% of the samples; on
+    the rest a one-ulp difference of a pre-activation flipped a binary16 rounding, bounded by 2e-3."""
     rng = np.random.default_rng(6)
-    for _ in range(40):
+    close = 0
+    n = 60
+    for _ in range(n):
         dims = [16, 64, 64, 64, 9]
         ws = [(rng.standard_normal((i, o)) * np.sqrt(2 / i)).astype(np.float16) for i, o in zip(dims[:-1], dims[1:])]
         bs = [rng.uniform(-0.1, 0.1, o).astype(np.float16) for o in dims[1:]]
         x = rng.uniform(-1, 1, 16).astype(np.float32)
-        got = oracle.mlp_raw(ws, bs, x)
         ref = _torch_mlp(ws, bs, x)
+        with oracle.plain_definitions():
+            plain = oracle.mlp_raw(ws, bs, x)
+        assert np.max(np.abs(plain - ref) / np.abs(ref)) < 1e-6
+        got = oracle.mlp_raw(ws, bs, x)
         assert np.max(np.abs(got - ref)) < 2e-3
+        close += np.max(np.abs(got - ref) / np.abs(ref)) < 1e-5
+    assert close >= 0.9 * n, close
 
 
 def test_mlp_zero_weights_gives_half():
